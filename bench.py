@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""Benchmark: DRRs/sec fwd+bwd (200x200 detector, 512x512x133 CT) on B200.
+
+One STEP = the hot path over one batch of poses: for B poses per GPU, render
+the 200x200 DRRs (drr_forward), evaluate the reference's registration loss
+(neg-ZNCC vs a fixed DRR, metrics.py:71-91) and back-propagate to the pose
+(drr_backward + autograd through the 12-number frame) -- i.e. B x the
+reference's ``loss_and_gradient`` (gradients.py:61-69), config C2 of
+SURVEY.md 8(d) with the C4 pose sampling.  Poses shard across ranks with no
+collective in the loop (weak scaling); the CT is NCCL-broadcast once.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  Timing: CUDA events per step on the launching
+stream, L2 flushed (256 MiB write) between timed steps outside the events,
+max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SPACING = (0.703125, 0.703125, 2.5)
+DIMS = (512, 512, 133)
+H = W = 200
+PITCH = 3.6
+RHO = 300.0
+TRUTH = (RHO, math.pi / 2, math.pi / 2, 0.0, 0.0, 0.0, 0.0)
+WORKLOAD = ("C2: synthetic chest CT 512x512x133 @ (0.703125,0.703125,2.5) mm fp32, "
+            "200x200 detector @ 3.6 mm, rho=sdr=300 mm; per step B poses (narrow samples "
+            "around AP, seed 0) x [forward DRR + neg-ZNCC vs fixed DRR + backward to "
+            "(rotation, translation)]")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--batch", type=int, default=32, help="poses per GPU per step")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=0, help="poses for the CPU baseline (0: auto)")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in getattr(self, "lines", []):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def _ref_worker(args):
+    """One pose of the reference's loss_and_gradient (native backend, 1 core)."""
+    eta, fixed = args
+    from oracle.oracle import reference_module
+    dt = reference_module()
+    vol = _REF_STATE["vol"]
+    spec = _REF_STATE["spec"]
+    t0 = time.perf_counter()
+    rec = dt.loss_and_gradient(vol, dt.PoseParameters.from_vector(eta), spec, fixed,
+                               "neg_zncc", backend="native")
+    return time.perf_counter() - t0, float(rec.value)
+
+
+_REF_STATE = {}
+
+
+def _port_worker(args):
+    """Fallback when oracle/_ref is absent: the C oracle (port) fwd + bwd."""
+    eta, fixed = args
+    from oracle import oracle as O
+    st = _REF_STATE
+    t0 = time.perf_counter()
+    frame = O.pose_frame(eta, st["center"])
+    img = O.render(st["flat"], DIMS, SPACING, (0, 0, 0), frame, H, W, PITCH, PITCH)
+    _, pg = O.neg_zncc_value_and_grad(img, fixed)
+    O.render_backward(st["flat"], DIMS, SPACING, (0, 0, 0), frame, H, W, PITCH, PITCH, pg)
+    return time.perf_counter() - t0, 0.0
+
+
+def cpu_setup(vol_np):
+    """Reference inputs: the fp32 CT cast back to f64."""
+    from oracle.oracle import reference_module
+    dt = reference_module()
+    flat = vol_np.astype(np.float64).ravel(order="F")
+    center = tuple(0.5 * n * s for n, s in zip(DIMS, SPACING))
+    _REF_STATE.update(flat=flat, center=center)
+    if dt is not None:
+        vol = dt.Volume(DIMS, SPACING, (0.0, 0.0, 0.0), vol_np.astype(np.float64))
+        _REF_STATE.update(vol=vol, spec=dt.DetectorSpec.for_volume(vol, H, W, (PITCH, PITCH)))
+        fixed = dt.render(vol, dt.PoseParameters.from_vector(TRUTH), _REF_STATE["spec"]).values
+        return "reference", _ref_worker, fixed
+    from oracle import oracle as O
+    frame = O.pose_frame(np.asarray(TRUTH), center)
+    fixed = O.render(flat, DIMS, SPACING, (0, 0, 0), frame, H, W, PITCH, PITCH)
+    return "port", _port_worker, fixed
+
+
+def cpu_run(worker, poses, fixed, procs):
+    """Pose-sharded fork pool (the reference kernels hold the GIL)."""
+    import multiprocessing as mp
+    t0 = time.perf_counter()
+    if procs <= 1:
+        res = [worker((p, fixed)) for p in poses]
+    else:
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(worker, [(p, fixed) for p in poses], chunksize=1)
+    return time.perf_counter() - t0, res
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------- main
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from paper_2208_12737_b200 import synthetic
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        return run_reference(args, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2208_12737_b200 import (DRR, backward_frames, count_steps, pose_frames,
+                                       render_frames)
+    from paper_2208_12737_b200 import _lib
+    from paper_2208_12737_b200.metrics import neg_zncc
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # --- volume: built on rank 0, NCCL-broadcast once --------
+    if rank == 0:
+        vol_np = synthetic.chest_phantom(DIMS)
+        vol_t = torch.from_numpy(vol_np).to(dev)
+    else:
+        vol_np = None
+        vol_t = torch.empty(DIMS, dtype=torch.float32, device=dev)
+    if world > 1:
+        dist.broadcast(vol_t, src=0)
+    drr = DRR(vol_t, SPACING, sdr=RHO, height=H, delx=PITCH, device=dev, strict=False)
+    del vol_t
+
+    # --- poses: global batch sharded by rank, no comms in the loop -------
+    B = args.batch
+    all_poses = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, B * world, seed=0)
+    poses_np = all_poses[rank * B:(rank + 1) * B]
+    rot0 = torch.tensor(poses_np[:, 1:4], device=dev)
+    tra0 = torch.tensor(poses_np[:, 4:7], device=dev)
+    with torch.no_grad():
+        fixed = drr(torch.tensor(TRUTH[1:4], device=dev), torch.tensor(TRUTH[4:7], device=dev))
+    fixed_b = fixed.expand(B, H, W)
+
+    def step(rot, tra):
+        rot = rot.detach().requires_grad_(True)
+        tra = tra.detach().requires_grad_(True)
+        img = drr(rot, tra)
+        loss = neg_zncc(img, fixed_b)
+        loss.sum().backward()
+        return loss.detach(), rot.grad, tra.grad
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    # --- warmup + timed steps (device time, per-step events) -------------
+    for _ in range(max(args.warmup, 3)):
+        step(rot0, tra0)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(rot0, tra0)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    local_ms = float(np.mean(times))
+    t = torch.tensor([local_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item())
+    value = B * world / (ms_per_step / 1e3)
+
+    # --- e2e: public API with pinned host poses in, loss+grads out -------
+    h_rot = torch.tensor(poses_np[:, 1:4]).pin_memory()
+    h_tra = torch.tensor(poses_np[:, 4:7]).pin_memory()
+    h_out = torch.empty((B, 7), dtype=torch.float64).pin_memory()
+    e2e_times = []
+    for i in range(args.steps + 3):
+        flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rot = h_rot.to(dev, non_blocking=True)
+        tra = h_tra.to(dev, non_blocking=True)
+        loss, gr, gt = step(rot, tra)
+        h_out.copy_(torch.cat([loss[:, None], gr, gt], dim=1), non_blocking=True)
+        e1.record(stream)
+        e1.synchronize()
+        if i >= 3:
+            e2e_times.append(e0.elapsed_time(e1))
+    e = torch.tensor([float(np.mean(e2e_times))], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e, op=dist.ReduceOp.MAX)
+    e2e_value = B * world / (float(e.item()) / 1e3)
+
+    # --- roofline of the dominant kernel (k_backward) --------------------
+    frames = pose_frames(drr.pose_vectors(rot0, tra0), drr.isocenter).detach()
+    steps_used = count_steps(drr.volume, drr.detector, frames)
+    S = float(steps_used.double().sum().item())  # used voxel-steps in the batch
+    g_img = torch.randn((B, H, W), device=dev, dtype=torch.float32)
+    kt = {"bwd": [], "fwd": []}
+    for i in range(8):
+        flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        backward_frames(drr.volume, drr.detector, frames, g_img)
+        e1.record(stream)
+        flush.fill_(1.0)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e2.record(stream)
+        render_frames(drr.volume, drr.detector, frames)
+        e3.record(stream)
+        e3.synchronize()
+        if i >= 2:
+            kt["bwd"].append(e0.elapsed_time(e1))
+            kt["fwd"].append(e2.elapsed_time(e3))
+    bwd_ms = float(np.mean(kt["bwd"]))
+    fwd_ms = float(np.mean(kt["fwd"]))
+    bytes_bwd = 4.0 * S + 4.0 * B * H * W  # gathers + grad_img read
+    bytes_fwd = 4.0 * S + 4.0 * B * H * W  # gathers + image store
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    achieved_bwd = bytes_bwd / (bwd_ms / 1e3) / 1e9
+
+    # single-pose latency (C2 as configs[1] states it: one pose fwd+bwd)
+    one = []
+    for i in range(10):
+        flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rr = rot0[:1].detach().requires_grad_(True)
+        tt = tra0[:1].detach().requires_grad_(True)
+        neg_zncc(drr(rr, tt), fixed[None]).sum().backward()
+        e1.record(stream)
+        e1.synchronize()
+        if i >= 3:
+            one.append(e0.elapsed_time(e1))
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    clocks = clk.summary()
+    result = {
+        "metric": "DRRs/sec fwd+bwd (200x200 det, 512x512x133 CT)",
+        "value": value,
+        "unit": "DRR/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 geometry / fp32 CT gathers",
+        "data": "synthetic (chest-shaped CT phantom, SURVEY 8(d))",
+        "config": {"workload": WORKLOAD, "poses_per_gpu": B, "global_batch": B * world,
+                   "detector": [H, W], "ct": list(DIMS), "parallelism": f"pose-shard x{world}",
+                   "l2": "flushed (256 MiB write) between timed steps, outside the events"},
+        "e2e": {"value": e2e_value, "unit": "DRR/s",
+                "h2d_bytes_per_step": int(h_rot.numel() * 8 + h_tra.numel() * 8),
+                "d2h_bytes_per_step": int(h_out.numel() * 8)},
+        "gpu_launches": 3 * args.steps,
+        "roofline": {"bound": "hbm", "kernel": "k_backward (fused re-walk + frame reduction)",
+                     "achieved": achieved_bwd, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved_bwd / hbm_peak, "traffic": None,
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_bwd, "launch_ms": bwd_ms},
+        "kernels": {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+                    "voxel_steps_per_drr": S / B,
+                    "voxel_steps_per_s_fwd": S / (fwd_ms / 1e3),
+                    "fwd_achieved_gbs": bytes_fwd / (fwd_ms / 1e3) / 1e9},
+        "single_pose_fwd_bwd_ms": float(np.mean(one)),
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        vol_np = vol_np if vol_np is not None else synthetic.chest_phantom(DIMS)
+        kind, worker, fixed_np = cpu_setup(vol_np)
+        procs = os.cpu_count() or 1
+        n = args.cpu_sample or procs
+        poses = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, n, seed=1)
+        wall, res = cpu_run(worker, poses, fixed_np, procs)
+        result["cpu_baseline"] = {
+            "value": n / wall, "unit": "DRR/s", "cores": procs, "kind": kind,
+            "sample": f"{n} poses of C2 loss_and_gradient (neg-ZNCC, native backend, f64), "
+                      f"pose-sharded over {procs} fork processes; {wall:.1f} s wall; "
+                      f"CPU {cpu_model()}"}
+    print(json.dumps(result))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_reference(args, world):
+    """--impl reference: the reference's own CPU path (oracle/_ref, native
+    Cython backend) on this host's cores, same metric/config; rank 0 only."""
+    from paper_2208_12737_b200 import synthetic
+    vol_np = synthetic.chest_phantom(DIMS)
+    kind, worker, fixed_np = cpu_setup(vol_np)
+    procs = os.cpu_count() or 1
+    per_step = procs  # one pose per core per step
+    rng_seed = 0
+    times = []
+    for i in range(max(args.warmup, 3) + args.steps):
+        poses = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, per_step,
+                                       seed=rng_seed + i)
+        wall, _ = cpu_run(worker, poses, fixed_np, procs)
+        if i >= max(args.warmup, 3):
+            times.append(wall)
+    ms = 1e3 * float(np.mean(times))
+    value = per_step / (ms / 1e3)
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "DRRs/sec fwd+bwd (200x200 det, 512x512x133 CT)",
+        "value": value, "unit": "DRR/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "poses_per_step": per_step,
+                   "parallelism": f"{procs} host processes"},
+        "cpu_baseline": {"value": value, "unit": "DRR/s", "cores": procs, "kind": kind,
+                         "sample": f"{per_step} poses per step, pose-sharded fork pool; "
+                                   f"CPU {cpu_model()}"},
+        "e2e": {"value": value, "unit": "DRR/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

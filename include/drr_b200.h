@@ -1,0 +1,113 @@
+/*
+ * drr_b200.h -- C ABI of the B200-native vectorised-Siddon DRR renderer.
+ *
+ * Stateless, re-entrant, one device per call (the caller selects the device
+ * with cudaSetDevice / torch.cuda.device).  Every pointer argument named
+ * `d_*` is DEVICE memory; `stream` is a cudaStream_t passed as void*.  The
+ * library never allocates device memory: the backward pass's workspace size is
+ * queried with drr_backward_workspace_size and supplied by the caller.
+ * Functions return DRR_OK (0) or a negative status; drr_last_error() gives the
+ * message of the calling thread's last failure.
+ *
+ * What each entry point replaces in the reference (drrtrace, /root/reference):
+ *   drr_raysum               <- _kernels/_native.pyx:140-193 siddon_raysum
+ *                               (and jacobs_raysum, _native.pyx:285-382: the
+ *                               GPU walk is already incremental)
+ *   drr_raysum_endpoint_grad <- _kernels/_native.pyx:196-282 siddon_raysum_grad
+ *                               (reverse-mode form: dE/ds, dE/dp per ray; the
+ *                               host shim contracts them with the T tangents)
+ *   drr_forward              <- raytrace.py:132-142 render() fused with
+ *                               geometry.py:152-175 detector_grid()
+ *   drr_backward             <- gradients.py:45-69 render_with_gradient +
+ *                               the pixel_grad @ d_image reduction, in reverse
+ *                               mode down to the 12-number frame (s, c, e1, e2)
+ *   drr_count_steps          <- _kernels/python_ref.py:191-201 ray_structure
+ *                               (number of used voxel-steps per ray)
+ */
+#ifndef DRR_B200_H
+#define DRR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DRR_OK 0
+#define DRR_ERR_INVALID_ARGUMENT -1   /* -> drrtrace InvalidArgumentError   */
+#define DRR_ERR_CUDA -2               /* launch / runtime failure            */
+#define DRR_ERR_GRADIENT_UNDEFINED -3 /* -> drrtrace GradientUndefinedError  */
+#define DRR_ERR_WORKSPACE -4          /* workspace too small                 */
+
+/* Volume element type of d_vol. */
+#define DRR_VOL_F32 0 /* product layout: fp32 densities, x-fastest        */
+#define DRR_VOL_F64 1 /* drop-in for the reference's float64 flat volume  */
+
+/* Axis-aligned voxel grid: dims[a] voxels of spacing[a] mm, planes at
+ * origin[a] + k*spacing[a], k = 0..dims[a]   (volume.py:24-60). */
+typedef struct drr_grid {
+  int64_t dims[3];
+  double spacing[3];
+  double origin[3];
+} drr_grid;
+
+/* Detector: H x W pixels, pitch_x along W, pitch_y along H (geometry.py:71-97,
+ * 152-157).  Pixel (h, w) sits at c + a_h e1 + a_w e2. */
+typedef struct drr_detector {
+  int32_t height;
+  int32_t width;
+  double pitch_x;
+  double pitch_y;
+} drr_detector;
+
+/* Frames: B x 12 float64, per pose (s[3], c[3], e1[3], e2[3]) in volume
+ * coordinates (isocenter already added), geometry.py:120-149. */
+
+const char *drr_last_error(void);
+int drr_version(void);
+
+/* Energies of explicit rays from one source: out[r] = |p_r - s| sum seg V.
+ * d_src: 3 doubles, d_pix: N x 3 doubles, d_out: N doubles. */
+int drr_raysum(const void *d_vol, int vol_dtype, const drr_grid *grid,
+               const double *d_src, const double *d_pix, int64_t n_rays,
+               double *d_out, void *stream);
+
+/* Same walk, plus the reverse-mode endpoint derivatives dE/ds and dE/dp
+ * (N x 3 each).  d_out is bitwise equal to drr_raysum's. */
+int drr_raysum_endpoint_grad(const void *d_vol, int vol_dtype,
+                             const drr_grid *grid, const double *d_src,
+                             const double *d_pix, int64_t n_rays,
+                             double *d_out, double *d_dEds, double *d_dEdp,
+                             void *stream);
+
+/* Batched DRR forward: pixel rays generated in-kernel from the frames.
+ * d_img: B x H x W, float32 (img_dtype 0) or float64 (img_dtype 1). */
+int drr_forward(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                const double *d_frames, int32_t n_poses,
+                const drr_detector *det, void *d_img, int img_dtype,
+                void *stream);
+
+size_t drr_backward_workspace_size(int32_t n_poses, const drr_detector *det);
+
+/* Batched backward: d_grad_img B x H x W (float32 or float64 per
+ * grad_dtype) -> d_grad_frames B x 12 float64, reduced over pixels in a fixed
+ * order (bit-reproducible; no atomics).  Optionally also writes the image
+ * (d_img may be NULL; same dtype rule as drr_forward's img_dtype). */
+int drr_backward(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                 const double *d_frames, int32_t n_poses,
+                 const drr_detector *det, const void *d_grad_img,
+                 int grad_dtype, double *d_grad_frames, void *d_img,
+                 int img_dtype, void *d_workspace, size_t workspace_bytes,
+                 void *stream);
+
+/* Used voxel-steps per ray (segments longer than 1e-12), B x H x W int32. */
+int drr_count_steps(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                    const double *d_frames, int32_t n_poses,
+                    const drr_detector *det, int32_t *d_steps, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DRR_B200_H */

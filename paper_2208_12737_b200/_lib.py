@@ -1,0 +1,121 @@
+"""ctypes binding of the C ABI in ``include/drr_b200.h``.
+
+The shared library ``_lib/libdrr_b200.so`` is built in-tree by
+``paper_2208_12737_b200.build`` (nvcc, sm_100a).  There is no fallback: if the
+library is missing every entry point raises, so a GPU run can never silently
+route through anything but the CUDA kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import GradientUndefinedError, InvalidArgumentError, KernelError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libdrr_b200.so")
+
+DRR_OK = 0
+DRR_ERR_INVALID_ARGUMENT = -1
+DRR_ERR_CUDA = -2
+DRR_ERR_GRADIENT_UNDEFINED = -3
+DRR_ERR_WORKSPACE = -4
+
+DRR_VOL_F32 = 0
+DRR_VOL_F64 = 1
+
+# Every symbol include/drr_b200.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "drr_last_error",
+    "drr_version",
+    "drr_raysum",
+    "drr_raysum_endpoint_grad",
+    "drr_forward",
+    "drr_backward_workspace_size",
+    "drr_backward",
+    "drr_count_steps",
+)
+
+
+class DrrGrid(ctypes.Structure):
+    _fields_ = [("dims", ctypes.c_int64 * 3),
+                ("spacing", ctypes.c_double * 3),
+                ("origin", ctypes.c_double * 3)]
+
+
+class DrrDetector(ctypes.Structure):
+    _fields_ = [("height", ctypes.c_int32),
+                ("width", ctypes.c_int32),
+                ("pitch_x", ctypes.c_double),
+                ("pitch_y", ctypes.c_double)]
+
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_sz = ctypes.c_size_t
+_GP = ctypes.POINTER(DrrGrid)
+_DP = ctypes.POINTER(DrrDetector)
+
+_SIGNATURES = {
+    "drr_last_error": ([], ctypes.c_char_p),
+    "drr_version": ([], _int),
+    "drr_raysum": ([_vp, _int, _GP, _vp, _vp, _i64, _vp, _vp], _int),
+    "drr_raysum_endpoint_grad": ([_vp, _int, _GP, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _int),
+    "drr_forward": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp], _int),
+    "drr_backward_workspace_size": ([_i32, _DP], _sz),
+    "drr_backward": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp, _vp, _int, _vp, _sz, _vp], _int),
+    "drr_count_steps": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load (once) and type the native library; raises if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(
+            f"native DRR library not built: {path} is missing; run "
+            "`python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (args, res) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    """Map a C-ABI status to the reference's exception classes."""
+    if rc == DRR_OK:
+        return
+    msg = load().drr_last_error().decode("utf-8", "replace")
+    if rc == DRR_ERR_INVALID_ARGUMENT:
+        raise InvalidArgumentError(msg)
+    if rc == DRR_ERR_GRADIENT_UNDEFINED:
+        raise GradientUndefinedError(msg)
+    raise KernelError(f"drr status {rc}: {msg}")
+
+
+def make_grid(dims, spacing, origin) -> DrrGrid:
+    g = DrrGrid()
+    for a in range(3):
+        g.dims[a] = int(dims[a])
+        g.spacing[a] = float(spacing[a])
+        g.origin[a] = float(origin[a])
+    return g
+
+
+def make_detector(height, width, pitch_x, pitch_y) -> DrrDetector:
+    d = DrrDetector()
+    d.height = int(height)
+    d.width = int(width)
+    d.pitch_x = float(pitch_x)
+    d.pitch_y = float(pitch_y)
+    return d

@@ -1,0 +1,539 @@
+// drr_kernels.cu -- sm_100a kernels and the extern "C" ABI of include/drr_b200.h.
+//
+// Kernels (all gather-bound; no dense contraction, so no tensor cores):
+//   k_forward      one thread per detector pixel of a B x H x W batch; the
+//                  pixel ray is generated in-kernel from the pose frame
+//                  (geometry.py:152-175 fused with _native.pyx:140-193);
+//                  CTAs cover 16 x 8 pixel tiles whose warps are 8 x 4
+//                  quads, so neighbouring rays gather neighbouring voxels.
+//   k_backward     the fused re-walk: per pixel dE/ds, dE/dp (reverse mode),
+//                  weighted by the upstream pixel gradient and reduced per
+//                  CTA to the 12 frame gradients in a fixed order.
+//   k_reduce_frames  fixed-order second pass over the CTA partials (no atomics
+//                  anywhere, so gradients are bit-reproducible: SPEC.md:289).
+//   k_raysum / k_raysum_grad   explicit-ray forms for the kernel-protocol
+//                  backend (the reference's _kernels plugin boundary).
+//   k_count        used voxel-steps per ray (roofline denominator).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include "../../include/drr_b200.h"
+#include "siddon_walk.cuh"
+
+namespace drr {
+
+constexpr int kTileW = 16;
+constexpr int kTileH = 8;
+constexpr int kThreads = kTileW * kTileH;  // 4 warps, each an 8 x 4 quad
+constexpr int kFrameGrads = 12;
+
+// Lane -> pixel inside a 16 x 8 CTA tile: warp w covers the 8 x 4 quad
+// (w & 1, w >> 1); lanes are row-major inside the quad.
+__device__ __forceinline__ void tile_pixel(int& h, int& w) {
+  const int t = threadIdx.x;
+  const int warp = t >> 5, lane = t & 31;
+  w = blockIdx.x * kTileW + (warp & 1) * 8 + (lane & 7);
+  h = blockIdx.y * kTileH + (warp >> 1) * 4 + (lane >> 3);
+}
+
+struct DetDev {
+  int H, W;
+  double pitch_x, pitch_y;
+  double half_h, half_w;  // (H-1)/2.0, (W-1)/2.0   (geometry.py:155-156)
+};
+
+// Pixel position (c + a_h e1) + a_w e2 in numpy's evaluation order
+// (geometry.py:171-174); the TU is built --fmad=false, so this rounds
+// exactly like numpy.
+__device__ __forceinline__ void pixel_ray(const double* __restrict__ f,
+                                          const DetDev& det, int h, int w,
+                                          double* s, double* p, double& ah,
+                                          double& aw) {
+  ah = (static_cast<double>(h) - det.half_h) * det.pitch_y;
+  aw = (static_cast<double>(w) - det.half_w) * det.pitch_x;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    s[a] = __ldg(f + a);
+    p[a] = (__ldg(f + 3 + a) + ah * __ldg(f + 6 + a)) + aw * __ldg(f + 9 + a);
+  }
+}
+
+__device__ __forceinline__ double ray_length(const Ray& r) {
+  return sqrt(r.d[0] * r.d[0] + r.d[1] * r.d[1] + r.d[2] * r.d[2]);
+}
+
+template <typename OT>
+__device__ __forceinline__ void store_out(OT* p, double v) {
+  *p = static_cast<OT>(v);
+}
+
+// ---------------------------------------------------------------- forward
+template <typename VT, typename OT>
+__global__ void __launch_bounds__(kThreads)
+    k_forward(const VT* __restrict__ vol, const GridDev g,
+              const double* __restrict__ frames, const DetDev det,
+              OT* __restrict__ img) {
+  int h, w;
+  tile_pixel(h, w);
+  if (h >= det.H || w >= det.W) return;
+  const int b = blockIdx.z;
+  double s[3], p[3], ah, aw;
+  pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
+  Ray r;
+  ray_setup(g, s, p, r);
+  double e = 0.0;
+  if (r.hit) {
+    SumVisitor vis;
+    walk<VT, false>(vol, g, r, vis);
+    e = ray_length(r) * vis.acc;
+  }
+  store_out(img + (static_cast<size_t>(b) * det.H + h) * det.W + w, e);
+}
+
+template <typename VT>
+__global__ void __launch_bounds__(kThreads)
+    k_count(const VT* __restrict__ vol, const GridDev g,
+            const double* __restrict__ frames, const DetDev det,
+            int* __restrict__ steps) {
+  int h, w;
+  tile_pixel(h, w);
+  if (h >= det.H || w >= det.W) return;
+  const int b = blockIdx.z;
+  double s[3], p[3], ah, aw;
+  pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
+  Ray r;
+  ray_setup(g, s, p, r);
+  int n = 0;
+  if (r.hit) {
+    CountVisitor vis;
+    walk<VT, false>(vol, g, r, vis);
+    n = vis.steps;
+  }
+  steps[(static_cast<size_t>(b) * det.H + h) * det.W + w] = n;
+}
+
+// Endpoint gradients of one ray from the reverse-mode visitor
+// (see orc_raysum_endpoint_grad in oracle/siddon_oracle.c for the algebra).
+__device__ __forceinline__ void endpoint_grads(const Ray& r,
+                                               const GradVisitor& v, double L,
+                                               double* dEds, double* dEdp) {
+  const double G[3] = {v.G0, v.G1, v.G2};
+  const double Hh[3] = {v.H0, v.H1, v.H2};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double gs = 0.0, gp = 0.0;
+    if (r.d[a] != 0.0) {
+      gs = L * (Hh[a] - G[a]) / r.d[a];
+      gp = -L * Hh[a] / r.d[a];
+    }
+    const double lt = r.d[a] / L * v.acc;
+    dEds[a] = gs - lt;
+    dEdp[a] = gp + lt;
+  }
+}
+
+// --------------------------------------------------------------- backward
+template <typename VT, typename GT, typename OT>
+__global__ void __launch_bounds__(kThreads)
+    k_backward(const VT* __restrict__ vol, const GridDev g,
+               const double* __restrict__ frames, const DetDev det,
+               const GT* __restrict__ grad_img, OT* __restrict__ img,
+               double* __restrict__ partials) {
+  int h, w;
+  tile_pixel(h, w);
+  const int b = blockIdx.z;
+  double acc12[kFrameGrads];
+#pragma unroll
+  for (int k = 0; k < kFrameGrads; ++k) acc12[k] = 0.0;
+  if (h < det.H && w < det.W) {
+    double s[3], p[3], ah, aw;
+    pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
+    const size_t pix = (static_cast<size_t>(b) * det.H + h) * det.W + w;
+    const double gpx = static_cast<double>(grad_img[pix]);
+    Ray r;
+    ray_setup(g, s, p, r);
+    double e = 0.0;
+    if (r.hit) {
+      GradVisitor vis;
+      walk<VT, true>(vol, g, r, vis);
+      const double L = ray_length(r);
+      e = L * vis.acc;
+      double dEds[3], dEdp[3];
+      endpoint_grads(r, vis, L, dEds, dEdp);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        acc12[a] = gpx * dEds[a];
+        acc12[3 + a] = gpx * dEdp[a];
+        acc12[6 + a] = gpx * ah * dEdp[a];
+        acc12[9 + a] = gpx * aw * dEdp[a];
+      }
+    }
+    if (img != nullptr) store_out(img + pix, e);
+  }
+  // Fixed-order CTA reduction: xor-butterfly inside each warp, then warps in
+  // index order.
+#pragma unroll
+  for (int k = 0; k < kFrameGrads; ++k) {
+    double v = acc12[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    acc12[k] = v;
+  }
+  __shared__ double warp_part[kThreads / 32][kFrameGrads];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kFrameGrads; ++k) warp_part[warp][k] = acc12[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < kFrameGrads) {
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kThreads / 32; ++q) v += warp_part[q][threadIdx.x];
+    const int blocks_per_pose = gridDim.x * gridDim.y;
+    const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+    partials[(static_cast<size_t>(b) * blocks_per_pose + blk) * kFrameGrads +
+             threadIdx.x] = v;
+  }
+}
+
+// One CTA per pose: each thread sums a fixed strided subset of the CTA
+// partials, then a fixed shared-memory tree.
+constexpr int kReduceThreads = 128;
+__global__ void __launch_bounds__(kReduceThreads)
+    k_reduce_frames(const double* __restrict__ partials, int blocks_per_pose,
+                    double* __restrict__ grad_frames) {
+  const int b = blockIdx.x;
+  __shared__ double sm[kReduceThreads][kFrameGrads + 1];
+  double v[kFrameGrads];
+#pragma unroll
+  for (int k = 0; k < kFrameGrads; ++k) v[k] = 0.0;
+  const double* base = partials + static_cast<size_t>(b) * blocks_per_pose * kFrameGrads;
+  for (int j = threadIdx.x; j < blocks_per_pose; j += kReduceThreads) {
+#pragma unroll
+    for (int k = 0; k < kFrameGrads; ++k) v[k] += base[j * kFrameGrads + k];
+  }
+#pragma unroll
+  for (int k = 0; k < kFrameGrads; ++k) sm[threadIdx.x][k] = v[k];
+  __syncthreads();
+  for (int stride = kReduceThreads / 2; stride > 0; stride >>= 1) {
+    if (threadIdx.x < stride) {
+#pragma unroll
+      for (int k = 0; k < kFrameGrads; ++k)
+        sm[threadIdx.x][k] += sm[threadIdx.x + stride][k];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < kFrameGrads)
+    grad_frames[b * kFrameGrads + threadIdx.x] = sm[0][threadIdx.x];
+}
+
+// ----------------------------------------------------------- explicit rays
+constexpr int kRayThreads = 128;
+
+template <typename VT>
+__global__ void __launch_bounds__(kRayThreads)
+    k_raysum(const VT* __restrict__ vol, const GridDev g,
+             const double* __restrict__ src, const double* __restrict__ pix,
+             int64_t n_rays, double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_rays) return;
+  double s[3] = {__ldg(src), __ldg(src + 1), __ldg(src + 2)};
+  double p[3] = {__ldg(pix + 3 * i), __ldg(pix + 3 * i + 1), __ldg(pix + 3 * i + 2)};
+  Ray r;
+  ray_setup(g, s, p, r);
+  double e = 0.0;
+  if (r.hit) {
+    SumVisitor vis;
+    walk<VT, false>(vol, g, r, vis);
+    e = ray_length(r) * vis.acc;
+  }
+  out[i] = e;
+}
+
+template <typename VT>
+__global__ void __launch_bounds__(kRayThreads)
+    k_raysum_grad(const VT* __restrict__ vol, const GridDev g,
+                  const double* __restrict__ src,
+                  const double* __restrict__ pix, int64_t n_rays,
+                  double* __restrict__ out, double* __restrict__ dEds,
+                  double* __restrict__ dEdp) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_rays) return;
+  double s[3] = {__ldg(src), __ldg(src + 1), __ldg(src + 2)};
+  double p[3] = {__ldg(pix + 3 * i), __ldg(pix + 3 * i + 1), __ldg(pix + 3 * i + 2)};
+  Ray r;
+  ray_setup(g, s, p, r);
+  double e = 0.0, gs[3] = {0.0, 0.0, 0.0}, gp[3] = {0.0, 0.0, 0.0};
+  if (r.hit) {
+    GradVisitor vis;
+    walk<VT, true>(vol, g, r, vis);
+    const double L = ray_length(r);
+    e = L * vis.acc;
+    endpoint_grads(r, vis, L, gs, gp);
+  }
+  out[i] = e;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    dEds[3 * i + a] = gs[a];
+    dEdp[3 * i + a] = gp[a];
+  }
+}
+
+}  // namespace drr
+
+// =================================================================== C ABI
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(DRR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return DRR_OK;
+}
+
+int make_grid(const drr_grid* in, drr::GridDev& g) {
+  if (in == nullptr) return fail(DRR_ERR_INVALID_ARGUMENT, "grid is NULL");
+  int64_t total = 1;
+  for (int a = 0; a < 3; ++a) {
+    if (in->dims[a] < 1)
+      return fail(DRR_ERR_INVALID_ARGUMENT, "dims must be >= 1, got %lld on axis %d",
+                  (long long)in->dims[a], a);
+    if (!(in->spacing[a] > 0.0) || !isfinite(in->spacing[a]))
+      return fail(DRR_ERR_INVALID_ARGUMENT, "spacing must be positive, got %g on axis %d",
+                  in->spacing[a], a);
+    if (!isfinite(in->origin[a]))
+      return fail(DRR_ERR_INVALID_ARGUMENT, "origin must be finite");
+    total *= in->dims[a];
+  }
+  if (total >= (int64_t(1) << 31))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "volume has %lld voxels; limit is 2^31-1",
+                (long long)total);
+  for (int a = 0; a < 3; ++a) {
+    g.n[a] = static_cast<int>(in->dims[a]);
+    g.sp[a] = in->spacing[a];
+    g.o[a] = in->origin[a];
+    // Same expression as _native.pyx:34 (host double arithmetic is IEEE;
+    // built without FMA contraction).
+    volatile double prod = static_cast<double>(in->dims[a]) * in->spacing[a];
+    g.hi[a] = in->origin[a] + prod;
+  }
+  g.stride[0] = 1;
+  g.stride[1] = g.n[0];
+  g.stride[2] = g.n[0] * g.n[1];
+  g.total = static_cast<int>(total);
+  return DRR_OK;
+}
+
+int make_det(const drr_detector* in, drr::DetDev& d) {
+  if (in == nullptr) return fail(DRR_ERR_INVALID_ARGUMENT, "detector is NULL");
+  if (in->height < 1 || in->width < 1)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "detector must be at least 1x1, got %dx%d",
+                in->height, in->width);
+  if (!(in->pitch_x > 0.0) || !(in->pitch_y > 0.0) || !isfinite(in->pitch_x) ||
+      !isfinite(in->pitch_y))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "pixel pitch must be positive");
+  d.H = in->height;
+  d.W = in->width;
+  d.pitch_x = in->pitch_x;
+  d.pitch_y = in->pitch_y;
+  d.half_h = static_cast<double>(in->height - 1) / 2.0;
+  d.half_w = static_cast<double>(in->width - 1) / 2.0;
+  return DRR_OK;
+}
+
+dim3 pose_grid(const drr::DetDev& d, int n_poses) {
+  return dim3((d.W + drr::kTileW - 1) / drr::kTileW,
+              (d.H + drr::kTileH - 1) / drr::kTileH, n_poses);
+}
+
+template <typename VT, typename GT>
+void launch_backward(const VT* vol, const drr::GridDev& g,
+                            const double* frames, const drr::DetDev& d,
+                            int n_poses, const GT* grad, void* img,
+                            int img_dtype, double* partials, cudaStream_t st) {
+  const dim3 grd = pose_grid(d, n_poses);
+  if (img_dtype == 1)
+    drr::k_backward<VT, GT, double><<<grd, drr::kThreads, 0, st>>>(
+        vol, g, frames, d, grad, static_cast<double*>(img), partials);
+  else
+    drr::k_backward<VT, GT, float><<<grd, drr::kThreads, 0, st>>>(
+        vol, g, frames, d, grad, static_cast<float*>(img), partials);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* drr_last_error(void) { return g_err; }
+
+int drr_version(void) { return 1; }
+
+int drr_raysum(const void* d_vol, int vol_dtype, const drr_grid* grid,
+               const double* d_src, const double* d_pix, int64_t n_rays,
+               double* d_out, void* stream) {
+  drr::GridDev g;
+  int rc = make_grid(grid, g);
+  if (rc) return rc;
+  if (n_rays < 0) return fail(DRR_ERR_INVALID_ARGUMENT, "n_rays < 0");
+  if (n_rays == 0) return DRR_OK;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const unsigned blocks = static_cast<unsigned>((n_rays + drr::kRayThreads - 1) / drr::kRayThreads);
+  if (vol_dtype == DRR_VOL_F32)
+    drr::k_raysum<float><<<blocks, drr::kRayThreads, 0, st>>>(
+        static_cast<const float*>(d_vol), g, d_src, d_pix, n_rays, d_out);
+  else if (vol_dtype == DRR_VOL_F64)
+    drr::k_raysum<double><<<blocks, drr::kRayThreads, 0, st>>>(
+        static_cast<const double*>(d_vol), g, d_src, d_pix, n_rays, d_out);
+  else
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
+  return check_launch("drr_raysum");
+}
+
+int drr_raysum_endpoint_grad(const void* d_vol, int vol_dtype,
+                             const drr_grid* grid, const double* d_src,
+                             const double* d_pix, int64_t n_rays,
+                             double* d_out, double* d_dEds, double* d_dEdp,
+                             void* stream) {
+  drr::GridDev g;
+  int rc = make_grid(grid, g);
+  if (rc) return rc;
+  if (n_rays < 0) return fail(DRR_ERR_INVALID_ARGUMENT, "n_rays < 0");
+  if (n_rays == 0) return DRR_OK;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const unsigned blocks = static_cast<unsigned>((n_rays + drr::kRayThreads - 1) / drr::kRayThreads);
+  if (vol_dtype == DRR_VOL_F32)
+    drr::k_raysum_grad<float><<<blocks, drr::kRayThreads, 0, st>>>(
+        static_cast<const float*>(d_vol), g, d_src, d_pix, n_rays, d_out, d_dEds, d_dEdp);
+  else if (vol_dtype == DRR_VOL_F64)
+    drr::k_raysum_grad<double><<<blocks, drr::kRayThreads, 0, st>>>(
+        static_cast<const double*>(d_vol), g, d_src, d_pix, n_rays, d_out, d_dEds, d_dEdp);
+  else
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
+  return check_launch("drr_raysum_endpoint_grad");
+}
+
+int drr_forward(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                const double* d_frames, int32_t n_poses,
+                const drr_detector* det, void* d_img, int img_dtype,
+                void* stream) {
+  drr::GridDev g;
+  drr::DetDev d;
+  int rc = make_grid(grid, g);
+  if (rc) return rc;
+  rc = make_det(det, d);
+  if (rc) return rc;
+  if (n_poses < 0 || n_poses > 65535)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
+  if (n_poses == 0) return DRR_OK;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const dim3 grd = pose_grid(d, n_poses);
+  if (vol_dtype == DRR_VOL_F32 && img_dtype == 0)
+    drr::k_forward<float, float><<<grd, drr::kThreads, 0, st>>>(
+        static_cast<const float*>(d_vol), g, d_frames, d, static_cast<float*>(d_img));
+  else if (vol_dtype == DRR_VOL_F32 && img_dtype == 1)
+    drr::k_forward<float, double><<<grd, drr::kThreads, 0, st>>>(
+        static_cast<const float*>(d_vol), g, d_frames, d, static_cast<double*>(d_img));
+  else if (vol_dtype == DRR_VOL_F64 && img_dtype == 1)
+    drr::k_forward<double, double><<<grd, drr::kThreads, 0, st>>>(
+        static_cast<const double*>(d_vol), g, d_frames, d, static_cast<double*>(d_img));
+  else if (vol_dtype == DRR_VOL_F64 && img_dtype == 0)
+    drr::k_forward<double, float><<<grd, drr::kThreads, 0, st>>>(
+        static_cast<const double*>(d_vol), g, d_frames, d, static_cast<float*>(d_img));
+  else
+    return fail(DRR_ERR_INVALID_ARGUMENT, "bad dtypes vol=%d img=%d", vol_dtype, img_dtype);
+  return check_launch("drr_forward");
+}
+
+size_t drr_backward_workspace_size(int32_t n_poses, const drr_detector* det) {
+  drr::DetDev d;
+  if (make_det(det, d) || n_poses < 0) return 0;
+  const dim3 grd = pose_grid(d, 1);
+  return static_cast<size_t>(n_poses) * grd.x * grd.y * drr::kFrameGrads * sizeof(double);
+}
+
+int drr_backward(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                 const double* d_frames, int32_t n_poses,
+                 const drr_detector* det, const void* d_grad_img,
+                 int grad_dtype, double* d_grad_frames, void* d_img,
+                 int img_dtype, void* d_workspace, size_t workspace_bytes,
+                 void* stream) {
+  drr::GridDev g;
+  drr::DetDev d;
+  int rc = make_grid(grid, g);
+  if (rc) return rc;
+  rc = make_det(det, d);
+  if (rc) return rc;
+  if (n_poses < 0 || n_poses > 65535)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
+  if (n_poses == 0) return DRR_OK;
+  const size_t need = drr_backward_workspace_size(n_poses, det);
+  if (workspace_bytes < need || d_workspace == nullptr)
+    return fail(DRR_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
+  if ((img_dtype != 0 && img_dtype != 1) || (grad_dtype != 0 && grad_dtype != 1))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "bad dtypes grad=%d img=%d", grad_dtype, img_dtype);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* partials = static_cast<double*>(d_workspace);
+  if (vol_dtype == DRR_VOL_F32) {
+    const float* vol = static_cast<const float*>(d_vol);
+    if (grad_dtype == 0)
+      launch_backward(vol, g, d_frames, d, n_poses, static_cast<const float*>(d_grad_img), d_img, img_dtype, partials, st);
+    else
+      launch_backward(vol, g, d_frames, d, n_poses, static_cast<const double*>(d_grad_img), d_img, img_dtype, partials, st);
+  } else if (vol_dtype == DRR_VOL_F64) {
+    const double* vol = static_cast<const double*>(d_vol);
+    if (grad_dtype == 0)
+      launch_backward(vol, g, d_frames, d, n_poses, static_cast<const float*>(d_grad_img), d_img, img_dtype, partials, st);
+    else
+      launch_backward(vol, g, d_frames, d, n_poses, static_cast<const double*>(d_grad_img), d_img, img_dtype, partials, st);
+  } else {
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
+  }
+  rc = check_launch("drr_backward");
+  if (rc) return rc;
+  const dim3 grd = pose_grid(d, 1);
+  drr::k_reduce_frames<<<n_poses, drr::kReduceThreads, 0, st>>>(
+      partials, static_cast<int>(grd.x * grd.y), d_grad_frames);
+  return check_launch("drr_backward/reduce");
+}
+
+int drr_count_steps(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                    const double* d_frames, int32_t n_poses,
+                    const drr_detector* det, int32_t* d_steps, void* stream) {
+  drr::GridDev g;
+  drr::DetDev d;
+  int rc = make_grid(grid, g);
+  if (rc) return rc;
+  rc = make_det(det, d);
+  if (rc) return rc;
+  if (n_poses < 0 || n_poses > 65535)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
+  if (n_poses == 0) return DRR_OK;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const dim3 grd = pose_grid(d, n_poses);
+  if (vol_dtype == DRR_VOL_F32)
+    drr::k_count<float><<<grd, drr::kThreads, 0, st>>>(
+        static_cast<const float*>(d_vol), g, d_frames, d, d_steps);
+  else if (vol_dtype == DRR_VOL_F64)
+    drr::k_count<double><<<grd, drr::kThreads, 0, st>>>(
+        static_cast<const double*>(d_vol), g, d_frames, d, d_steps);
+  else
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
+  return check_launch("drr_count_steps");
+}
+
+}  // extern "C"

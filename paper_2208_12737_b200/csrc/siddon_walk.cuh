@@ -1,0 +1,316 @@
+// siddon_walk.cuh -- the per-ray incremental Siddon walk shared by every
+// kernel in drr_kernels.cu (forward, backward, step count, explicit rays).
+//
+// Semantics are those of the reference's vectorised Siddon kernel
+// (_native.pyx:140-193 / python_ref.py:130-138): the ray R(a) = s + a (p - s),
+// a in [amin, amax] from the slab rule clipped to [0, 1]; all plane crossings
+// a_k = (o + k sp - s) / d inside [amin, amax] are visited in ascending order
+// (ties -> lowest axis first); segments with seg <= 1e-12 are skipped; each
+// used segment adds seg * V[voxel(midpoint)]; E = |p - s| * sum.
+//
+// B200 design (not a port of the reference's sort-and-merge):
+//  * no crossing list is materialised -- each axis keeps only its NEXT plane
+//    index and crossing parameter, so a ray is O(1) registers and the walk is
+//    one pass over the voxels it touches;
+//  * every crossing parameter is bit-identical to the reference's
+//    (o + k*sp - s)/d: the division is replaced by one multiply by the
+//    correctly-rounded reciprocal plus one Markstein FMA correction, which is
+//    the correctly rounded quotient (checked against IEEE division);
+//  * the voxel of a segment comes from the next-plane indices (pure integer
+//    bookkeeping).  The reference floors the midpoint instead; the two agree
+//    whenever the midpoint is farther than the rounding noise from every
+//    plane, which `seg > T` certifies (T per ray, see ray_setup).  Segments
+//    that fail the test (near-ties, grazing and near-parallel rays) take the
+//    reference's exact floor/clamp path, so results stay bit-identical.
+//
+// The translation unit is compiled with --fmad=false: every a*b+c written
+// below rounds twice, exactly like the reference's C (built without -march,
+// so without FMA contraction).  FMAs that are wanted are explicit __fma_rn.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace drr {
+
+constexpr double kSegEps = 1e-12;  // _native.pyx:16
+constexpr int kConstLabel = 3;     // _native.pyx:17
+
+struct GridDev {
+  int n[3];
+  int stride[3];   // 1, nx, nx*ny
+  int total;       // nx*ny*nz (< 2^31, checked on the host)
+  double sp[3];
+  double o[3];
+  double hi[3];    // o + n*sp, as _native.pyx:34 computes it
+};
+
+template <typename VT>
+__device__ __forceinline__ double load_voxel(const VT* __restrict__ vol, int i) {
+  return static_cast<double>(__ldg(vol + i));
+}
+
+// Correctly rounded num / d given inv = RN(1/d) (Markstein correction).
+__device__ __forceinline__ double div_rn(double num, double d, double inv) {
+  const double q0 = __dmul_rn(num, inv);
+  const double r = __fma_rn(-q0, d, num);
+  return __fma_rn(r, inv, q0);
+}
+
+// Crossing parameter of plane k on one axis, reference operation order:
+// (o + k*sp - s) / d   (_native.pyx:105).
+__device__ __forceinline__ double plane_alpha(double o, double sp, int k,
+                                              double s, double d, double inv,
+                                              bool safe) {
+  const double num = (o + static_cast<double>(k) * sp) - s;
+  if (safe) return num / d;  // subnormal-scale direction: plain IEEE division
+  return div_rn(num, d, inv);
+}
+
+// The reference's midpoint voxel lookup, exactly (_native.pyx:68-82).
+__device__ __forceinline__ int exact_index(double s, double d, double mid,
+                                           double o, double sp, int n) {
+  const double f = floor((s + mid * d - o) / sp);
+  if (!(f >= 0.0)) return 0;  // also maps NaN to 0 like the reference's cast
+  if (f >= static_cast<double>(n)) return n - 1;
+  return static_cast<int>(f);
+}
+
+__device__ __forceinline__ int exact_voxel(const GridDev& g, double s0, double s1,
+                                        double s2, double d0, double d1,
+                                        double d2, double mid) {
+  const int i = exact_index(s0, d0, mid, g.o[0], g.sp[0], g.n[0]);
+  const int j = exact_index(s1, d1, mid, g.o[1], g.sp[1], g.n[1]);
+  const int k = exact_index(s2, d2, mid, g.o[2], g.sp[2], g.n[2]);
+  return i + g.n[0] * (j + g.n[1] * k);
+}
+
+struct Ray {
+  double s[3], d[3], inv[3];
+  double an[3];     // crossing parameter of the next plane per axis (+inf: none)
+  int kn[3];        // index of the next plane per axis
+  int st[3];        // +1 / -1 walking direction, 0 for a parallel axis
+  double amin, amax;
+  double T;         // fast-voxel threshold on seg (see ray_setup)
+  int lab_min, lab_max;
+  int flat;         // flat voxel index of the segment after `prev`
+  bool hit;
+  bool safe;        // some |d_a| so small that RN(1/d_a) overflows: use IEEE '/'
+};
+
+// Slab entry/exit, first-max/first-min labels over (x, y, z, clip):
+// _native.pyx:20-65.
+__device__ __forceinline__ void entry_exit(const GridDev& g, Ray& r) {
+  double cmin[3], cmax[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (r.d[a] == 0.0) {
+      const bool inside = (g.o[a] <= r.s[a]) && (r.s[a] <= g.hi[a]);
+      cmin[a] = inside ? -INFINITY : INFINITY;
+      cmax[a] = inside ? INFINITY : -INFINITY;
+    } else {
+      double a0 = (g.o[a] - r.s[a]) / r.d[a];
+      double a1 = (g.hi[a] - r.s[a]) / r.d[a];
+      if (a0 > a1) { const double t = a0; a0 = a1; a1 = t; }
+      cmin[a] = a0;
+      cmax[a] = a1;
+    }
+  }
+  // First-max over (x, y, z, clip=0) and first-min over (x, y, z, clip=1):
+  // strict comparisons keep the lowest label on ties.
+  double bmin = cmin[0], bmax = cmax[0];
+  int lmin = 0, lmax = 0;
+#pragma unroll
+  for (int a = 1; a < 3; ++a) {
+    if (cmin[a] > bmin) { bmin = cmin[a]; lmin = a; }
+    if (cmax[a] < bmax) { bmax = cmax[a]; lmax = a; }
+  }
+  if (0.0 > bmin) { bmin = 0.0; lmin = kConstLabel; }
+  if (1.0 < bmax) { bmax = 1.0; lmax = kConstLabel; }
+  r.lab_min = lmin;
+  r.amin = bmin;
+  r.lab_max = lmax;
+  r.amax = bmax;
+  r.hit = r.amin < r.amax;
+}
+
+// Per-ray setup: direction, entry/exit, first kept plane per axis, starting
+// voxel and the fast-path threshold T.
+__device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
+                                          const double* p, Ray& r) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    r.s[a] = s[a];
+    r.d[a] = p[a] - s[a];
+  }
+  entry_exit(g, r);
+  r.safe = false;
+  if (!r.hit) return;
+  int vox[3];
+  double T = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double d = r.d[a];
+    if (d == 0.0) {
+      // Constant index along a parallel axis: the reference evaluates
+      // floor(((s + mid*0) - o)/sp) = floor((s - o)/sp), then clamps.
+      r.st[a] = 0;
+      r.kn[a] = 0;
+      r.inv[a] = 0.0;
+      r.an[a] = INFINITY;
+      const double f = floor((r.s[a] - g.o[a]) / g.sp[a]);
+      vox[a] = !(f >= 0.0) ? 0 : (f >= (double)g.n[a] ? g.n[a] - 1 : (int)f);
+      continue;
+    }
+    const double inv = __drcp_rn(d);
+    if (!(fabs(inv) < 1e300)) r.safe = true;
+    const int st = d > 0.0 ? 1 : -1;
+    r.inv[a] = inv;
+    r.st[a] = st;
+    // First plane (in walking order) with alpha >= amin: estimate, then fix
+    // up with the exact crossing parameters (monotone in k).
+    const double t = (r.s[a] + r.amin * d - g.o[a]) / g.sp[a];
+    double kf = st > 0 ? ceil(t) : floor(t);
+    kf = fmin(fmax(kf, -1.0), (double)g.n[a] + 1.0);
+    int k = (int)kf;
+    const int n = g.n[a];
+    for (int it = 0; it < 64; ++it) {
+      const int kb = k - st;
+      if (kb >= 0 && kb <= n &&
+          plane_alpha(g.o[a], g.sp[a], kb, r.s[a], d, inv, true) >= r.amin) {
+        k = kb;
+        continue;
+      }
+      if (k >= 0 && k <= n &&
+          plane_alpha(g.o[a], g.sp[a], k, r.s[a], d, inv, true) < r.amin) {
+        k += st;
+        continue;
+      }
+      break;
+    }
+    r.kn[a] = k;
+    r.an[a] = (k >= 0 && k <= n)
+                  ? plane_alpha(g.o[a], g.sp[a], k, r.s[a], d, inv, true)
+                  : INFINITY;
+    vox[a] = st > 0 ? k - 1 : k;
+    // Fast-voxel certificate.  The reference's midpoint position and our
+    // crossing parameters carry rounding error below ~2^-50 * M voxels, with
+    // M the coordinate magnitude in voxel units.  A used segment's midpoint
+    // sits at least seg/2 * |d|/sp voxels from every a-plane, so
+    // seg > 2^-39 * (M + 1) * sp / |d| guarantees floor(midpoint) equals the
+    // next-plane bookkeeping with a 2^10 safety factor.
+    const double M = fabs(r.s[a]) + fabs(d) + fabs(g.o[a]) + fabs(g.hi[a]) +
+                     g.sp[a];
+    T = fmax(T, 0x1.0p-39 * M / fabs(d));
+  }
+  r.T = T;
+  r.flat = vox[0] + g.stride[1] * vox[1] + g.stride[2] * vox[2];
+}
+
+// Walks the ray, calling `on_segment(v, seg, prev, cur, lab_prev, lab_cur)`
+// for every used segment in ascending order and `on_crossing` bookkeeping in
+// the visitor.  Returns the raw sum acc (E = |d| * acc).
+//
+// Visitor interface:
+//   vis.segment(double v, double seg)        -- used segment, value v
+//   vis.crossing(int label, double alpha, double v_after)
+//       -- called once per crossing (entry first, exit last) with the value of
+//          the used segment that STARTS at it (0 when skipped); the visitor
+//          derives the crossing's reverse-mode coefficient from it.
+template <typename VT, bool kCrossings, typename Visitor>
+__device__ __forceinline__ void walk(const VT* __restrict__ vol,
+                                     const GridDev& g, Ray& r, Visitor& vis) {
+  double an0 = r.an[0], an1 = r.an[1], an2 = r.an[2];
+  int k0 = r.kn[0], k1 = r.kn[1], k2 = r.kn[2];
+  int flat = r.flat;
+  double prev = r.amin;
+  int lab_prev = r.lab_min;
+  const int total = g.total;
+  for (;;) {
+    double best = an0;
+    int sel = 0;
+    if (an1 < best) { best = an1; sel = 1; }
+    if (an2 < best) { best = an2; sel = 2; }
+    const bool last = !(best <= r.amax);
+    const double cur = last ? r.amax : best;
+    const double seg = cur - prev;
+    double v = 0.0;
+    if (seg > kSegEps) {
+      int idx = flat;
+      if (!(seg > r.T) || static_cast<unsigned>(flat) >= static_cast<unsigned>(total))
+        idx = exact_voxel(g, r.s[0], r.s[1], r.s[2], r.d[0], r.d[1], r.d[2],
+                          0.5 * (prev + cur));
+      v = load_voxel(vol, idx);
+      vis.segment(v, seg);
+    }
+    if (kCrossings) vis.crossing(lab_prev, prev, v);
+    prev = cur;
+    if (last) {
+      if (kCrossings) vis.crossing(r.lab_max, cur, 0.0);
+      break;
+    }
+    lab_prev = sel;
+    // Advance the selected axis to its next plane.
+    double o, sp, s, d, inv;
+    int k, st, n, df;
+    if (sel == 0) {
+      o = g.o[0]; sp = g.sp[0]; s = r.s[0]; d = r.d[0]; inv = r.inv[0];
+      k = k0; st = r.st[0]; n = g.n[0]; df = st;
+    } else if (sel == 1) {
+      o = g.o[1]; sp = g.sp[1]; s = r.s[1]; d = r.d[1]; inv = r.inv[1];
+      k = k1; st = r.st[1]; n = g.n[1]; df = st * g.stride[1];
+    } else {
+      o = g.o[2]; sp = g.sp[2]; s = r.s[2]; d = r.d[2]; inv = r.inv[2];
+      k = k2; st = r.st[2]; n = g.n[2]; df = st * g.stride[2];
+    }
+    k += st;
+    const double anew =
+        (k >= 0 && k <= n) ? plane_alpha(o, sp, k, s, d, inv, r.safe) : INFINITY;
+    flat += df;
+    if (sel == 0) { an0 = anew; k0 = k; }
+    else if (sel == 1) { an1 = anew; k1 = k; }
+    else { an2 = anew; k2 = k; }
+  }
+}
+
+// ---- visitors ----------------------------------------------------------
+
+struct SumVisitor {
+  double acc = 0.0;
+  __device__ __forceinline__ void segment(double v, double seg) {
+    acc = acc + seg * v;  // _native.pyx:187, no FMA (TU built --fmad=false)
+  }
+  __device__ __forceinline__ void crossing(int, double, double) {}
+};
+
+struct CountVisitor {
+  int steps = 0;
+  __device__ __forceinline__ void segment(double, double) { ++steps; }
+  __device__ __forceinline__ void crossing(int, double, double) {}
+};
+
+// Reverse mode: each crossing k on axis a carries the coefficient
+// c_k = v(segment ending at k) - v(segment starting at k); with
+// d alpha_k/ds_a = (alpha_k - 1)/d_a and d alpha_k/dp_a = -alpha_k/d_a the ray's
+// endpoint gradients need only G_a = sum c_k and H_a = sum c_k alpha_k.
+struct GradVisitor {
+  double acc = 0.0;
+  double pend = 0.0;  // value of the used segment ending at the next crossing
+  double G0 = 0.0, G1 = 0.0, G2 = 0.0, H0 = 0.0, H1 = 0.0, H2 = 0.0;
+  __device__ __forceinline__ void segment(double v, double seg) {
+    acc = acc + seg * v;
+  }
+  __device__ __forceinline__ void crossing(int label, double alpha,
+                                           double v_after) {
+    const double c = pend - v_after;
+    pend = v_after;
+    const double c0 = label == 0 ? c : 0.0;
+    const double c1 = label == 1 ? c : 0.0;
+    const double c2 = label == 2 ? c : 0.0;
+    G0 += c0; G1 += c1; G2 += c2;
+    H0 = __fma_rn(c0, alpha, H0);
+    H1 = __fma_rn(c1, alpha, H1);
+    H2 = __fma_rn(c2, alpha, H2);
+  }
+};
+
+}  // namespace drr

@@ -1,0 +1,234 @@
+"""The drop-in north-star API: ``DRR(volume, spacing, sdr, height, delx)``.
+
+``DRR`` is an ``nn.Module`` whose ``forward(rotation, translation)`` returns a
+differentiable (B, H, W) float32 image.  It is the batched, device-resident
+equivalent of the reference's ``render`` / ``render_with_gradient`` /
+``loss_and_gradient`` chain (``raytrace.py:132-142``, ``gradients.py:45-69``):
+
+* ``rotation`` = (theta, phi, gamma) radians and ``translation`` = the shift
+  (bx, by, bz) in mm relative to the isocentre (``geometry.py:24,142-143``);
+* ``sdr`` is rho, half the source-detector distance (``PAPER.md:144``);
+* ``delx`` (and ``dely``) is the pixel pitch; the isocentre is the volume
+  centre (``DetectorSpec.for_volume``, ``geometry.py:94-97``);
+* the volume is indexed [i, j, k] = (x, y, z) like ``Volume.data`` and kept
+  on the device as float32 in the reference's x-fastest flat layout
+  (``volume.py:77-79``).
+
+The image comes from ``drr_forward`` and its gradient from ``drr_backward``
+(one fused re-walk that reduces dL/d(frame) on the device); torch autograd only
+chains the 12 frame numbers to the pose (``geometry.pose_frames``).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import InvalidArgumentError
+from .geometry import check_gimbal, check_pose_vectors, pose_frames, volume_center
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _require_cuda(t: torch.Tensor, name: str) -> None:
+    if not t.is_cuda:
+        raise InvalidArgumentError(f"{name} must be a CUDA tensor (no CPU fallback)")
+
+
+class DeviceVolume:
+    """A CT volume resident in HBM: float32, x-fastest, plus its grid."""
+
+    def __init__(self, data, spacing, origin=(0.0, 0.0, 0.0), device=None,
+                 dtype=torch.float32):
+        spacing = tuple(float(s) for s in np.broadcast_to(np.asarray(spacing, dtype=np.float64), (3,)))
+        origin = tuple(float(s) for s in np.broadcast_to(np.asarray(origin, dtype=np.float64), (3,)))
+        if isinstance(data, torch.Tensor):
+            t = data.detach()
+        else:
+            t = torch.as_tensor(np.asarray(data))
+        if t.ndim != 3:
+            raise InvalidArgumentError(f"volume must be 3-D (nx, ny, nz), got shape {tuple(t.shape)}")
+        if any(n < 1 for n in t.shape):
+            raise InvalidArgumentError(f"dims must be >= 1, got {tuple(t.shape)}")
+        if any(not (s > 0 and np.isfinite(s)) for s in spacing):
+            raise InvalidArgumentError(f"spacing must be three positive reals, got {spacing}")
+        device = torch.device(device) if device is not None else torch.device("cuda")
+        self.dims = tuple(int(n) for n in t.shape)
+        self.spacing = spacing
+        self.origin = origin
+        self.dtype = dtype
+        # [i, j, k] -> x-fastest flat: memory order (k, j, i).
+        self.flat = t.to(device=device, dtype=dtype).permute(2, 1, 0).contiguous().reshape(-1)
+        self.vol_dtype = _lib.DRR_VOL_F32 if dtype == torch.float32 else _lib.DRR_VOL_F64
+        self.grid = _lib.make_grid(self.dims, self.spacing, self.origin)
+
+    @classmethod
+    def from_flat(cls, flat, dims, spacing, origin=(0.0, 0.0, 0.0), device=None,
+                  dtype=torch.float32):
+        """From an x-fastest flat array (the reference's ``flat_data()``)."""
+        arr = np.asarray(flat).reshape(tuple(int(n) for n in dims)[::-1])  # (nz, ny, nx)
+        return cls(np.transpose(arr, (2, 1, 0)), spacing, origin, device, dtype)
+
+    @property
+    def center(self):
+        return volume_center(self.dims, self.spacing, self.origin)
+
+    @property
+    def device(self):
+        return self.flat.device
+
+
+class Detector:
+    """H x W detector with pitch (x along W, y along H), geometry.py:71-97."""
+
+    def __init__(self, height: int, width: int, pitch_x: float, pitch_y: float | None = None):
+        pitch_y = pitch_x if pitch_y is None else pitch_y
+        if int(height) < 1 or int(width) < 1:
+            raise InvalidArgumentError(f"detector must be at least 1x1, got {height}x{width}")
+        if not (pitch_x > 0 and pitch_y > 0 and np.isfinite(pitch_x) and np.isfinite(pitch_y)):
+            raise InvalidArgumentError(f"pixel pitch must be positive, got {(pitch_x, pitch_y)}")
+        self.height, self.width = int(height), int(width)
+        self.pitch_x, self.pitch_y = float(pitch_x), float(pitch_y)
+        self.c = _lib.make_detector(self.height, self.width, self.pitch_x, self.pitch_y)
+
+
+def render_frames(vol: DeviceVolume, det: Detector, frames: torch.Tensor,
+                  out_dtype=torch.float32) -> torch.Tensor:
+    """(B, 12) float64 frames -> (B, H, W) images via ``drr_forward``."""
+    _require_cuda(frames, "frames")
+    frames = frames.detach().to(torch.float64).contiguous()
+    B = frames.shape[0]
+    img = torch.empty((B, det.height, det.width), dtype=out_dtype, device=frames.device)
+    lib = _lib.load()
+    _lib.check(lib.drr_forward(vol.flat.data_ptr(), vol.vol_dtype, vol.grid, frames.data_ptr(),
+                               B, det.c, img.data_ptr(), 1 if out_dtype == torch.float64 else 0,
+                               _stream_ptr(frames.device)))
+    return img
+
+
+def backward_frames(vol: DeviceVolume, det: Detector, frames: torch.Tensor,
+                    grad_img: torch.Tensor, want_image: bool = False):
+    """dL/d(frame) (B, 12) float64 for an upstream (B, H, W) pixel gradient."""
+    frames = frames.detach().to(torch.float64).contiguous()
+    if grad_img.dtype not in (torch.float32, torch.float64):
+        grad_img = grad_img.to(torch.float32)
+    grad_img = grad_img.contiguous()
+    B = frames.shape[0]
+    lib = _lib.load()
+    ws_bytes = lib.drr_backward_workspace_size(B, det.c)
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=frames.device)
+    grad_frames = torch.empty((B, 12), dtype=torch.float64, device=frames.device)
+    img = None
+    if want_image:
+        img = torch.empty((B, det.height, det.width), dtype=torch.float32, device=frames.device)
+    _lib.check(lib.drr_backward(
+        vol.flat.data_ptr(), vol.vol_dtype, vol.grid, frames.data_ptr(), B, det.c,
+        grad_img.data_ptr(), 1 if grad_img.dtype == torch.float64 else 0,
+        grad_frames.data_ptr(), img.data_ptr() if img is not None else None, 0,
+        ws.data_ptr(), ws_bytes, _stream_ptr(frames.device)))
+    return (grad_frames, img) if want_image else grad_frames
+
+
+def count_steps(vol: DeviceVolume, det: Detector, frames: torch.Tensor) -> torch.Tensor:
+    """Used voxel-steps per ray (B, H, W) int32 (python_ref.ray_structure's `use`)."""
+    frames = frames.detach().to(torch.float64).contiguous()
+    B = frames.shape[0]
+    steps = torch.empty((B, det.height, det.width), dtype=torch.int32, device=frames.device)
+    lib = _lib.load()
+    _lib.check(lib.drr_count_steps(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
+                                   frames.data_ptr(), B, det.c, steps.data_ptr(),
+                                   _stream_ptr(frames.device)))
+    return steps
+
+
+class _RenderFrames(torch.autograd.Function):
+    """frames (B, 12) -> image (B, H, W); backward = the fused CUDA re-walk."""
+
+    @staticmethod
+    def forward(ctx, frames, vol, det):
+        ctx.save_for_backward(frames)
+        ctx.vol, ctx.det = vol, det
+        return render_frames(vol, det, frames)
+
+    @staticmethod
+    def backward(ctx, grad_img):
+        (frames,) = ctx.saved_tensors
+        grad_frames = backward_frames(ctx.vol, ctx.det, frames, grad_img)
+        return grad_frames.to(frames.dtype), None, None
+
+
+def render_pose_vectors(vol: DeviceVolume, det: Detector, eta: torch.Tensor,
+                        isocenter=None) -> torch.Tensor:
+    """Differentiable render of (B, 7) pose vectors (rho, theta, phi, gamma, shift)."""
+    iso = vol.center if isocenter is None else isocenter
+    frames = pose_frames(eta.to(torch.float64), iso)
+    return _RenderFrames.apply(frames, vol, det)
+
+
+class DRR(torch.nn.Module):
+    """Differentiable DRR renderer: ``DRR(volume, spacing, sdr, height, delx)``.
+
+    ``forward(rotation, translation)`` takes (B, 3) or (3,) tensors and returns
+    (B, H, W) or (H, W) float32 images.  Gradients flow to rotation,
+    translation and (if given as a tensor to ``forward``) ``sdr``.
+    ``strict=True`` keeps the reference's validation (finite poses, and the
+    |sin phi| > 1e-6 gimbal guard when a gradient is requested,
+    ``gradients.py:39-42``); it synchronises with the device, so latency-bound
+    loops (and CUDA-graph capture) pass ``strict=False``.
+    """
+
+    def __init__(self, volume, spacing, sdr: float, height: int, delx: float,
+                 width: int | None = None, dely: float | None = None,
+                 origin=(0.0, 0.0, 0.0), isocenter=None, device=None,
+                 strict: bool = True):
+        super().__init__()
+        self.volume = DeviceVolume(volume, spacing, origin, device=device)
+        self.detector = Detector(height, width if width is not None else height, delx, dely)
+        if not (float(sdr) > 0 and np.isfinite(float(sdr))):
+            raise InvalidArgumentError(f"sdr must be positive, got {sdr}")
+        self.sdr = float(sdr)
+        self.isocenter = tuple(self.volume.center if isocenter is None else
+                               (float(v) for v in isocenter))
+        self.strict = strict
+
+    @property
+    def height(self):
+        return self.detector.height
+
+    @property
+    def width(self):
+        return self.detector.width
+
+    def pose_vectors(self, rotation, translation, sdr=None) -> torch.Tensor:
+        dev = self.volume.device
+        rot = torch.as_tensor(rotation, device=dev)
+        tra = torch.as_tensor(translation, device=dev)
+        if rot.ndim == 1:
+            rot = rot[None]
+        if tra.ndim == 1:
+            tra = tra[None]
+        if rot.shape[-1] != 3 or tra.shape[-1] != 3 or rot.shape[0] != tra.shape[0]:
+            raise InvalidArgumentError(
+                f"rotation/translation must be (B, 3), got {tuple(rot.shape)} / {tuple(tra.shape)}")
+        rot = rot.to(torch.float64)
+        tra = tra.to(torch.float64)
+        if sdr is None:
+            rho = torch.full((rot.shape[0], 1), self.sdr, dtype=torch.float64, device=dev)
+        else:
+            rho = torch.as_tensor(sdr, device=dev).to(torch.float64).reshape(-1, 1)
+            rho = rho.expand(rot.shape[0], 1)
+        return torch.cat([rho, rot, tra], dim=1)
+
+    def forward(self, rotation, translation, sdr=None):
+        single = torch.as_tensor(rotation).ndim == 1
+        eta = self.pose_vectors(rotation, translation, sdr)
+        if self.strict:
+            check_pose_vectors(eta.detach())
+            if torch.is_grad_enabled() and eta.requires_grad:
+                check_gimbal(eta.detach())
+        frames = pose_frames(eta, self.isocenter)
+        img = _RenderFrames.apply(frames, self.volume, self.detector)
+        return img[0] if single else img
