@@ -77,6 +77,9 @@ __global__ void __launch_bounds__(kThreads)
     k_forward(const VT* __restrict__ vol, const GridDev g,
               const double* __restrict__ frames, const DetDev det,
               OT* __restrict__ img) {
+  extern __shared__ double tab[];
+  build_plane_table(g, tab);
+  __syncthreads();
   int h, w;
   tile_pixel(h, w);
   if (h >= det.H || w >= det.W) return;
@@ -88,7 +91,7 @@ __global__ void __launch_bounds__(kThreads)
   double e = 0.0;
   if (r.hit) {
     SumVisitor vis;
-    walk<VT, false>(vol, g, r, vis);
+    walk<VT>(vol, g, tab, r, vis);
     e = ray_length(r) * vis.acc;
   }
   store_out(img + (static_cast<size_t>(b) * det.H + h) * det.W + w, e);
@@ -99,6 +102,9 @@ __global__ void __launch_bounds__(kThreads)
     k_count(const VT* __restrict__ vol, const GridDev g,
             const double* __restrict__ frames, const DetDev det,
             int* __restrict__ steps) {
+  extern __shared__ double tab[];
+  build_plane_table(g, tab);
+  __syncthreads();
   int h, w;
   tile_pixel(h, w);
   if (h >= det.H || w >= det.W) return;
@@ -110,7 +116,7 @@ __global__ void __launch_bounds__(kThreads)
   int n = 0;
   if (r.hit) {
     CountVisitor vis;
-    walk<VT, false>(vol, g, r, vis);
+    walk<VT>(vol, g, tab, r, vis);
     n = vis.steps;
   }
   steps[(static_cast<size_t>(b) * det.H + h) * det.W + w] = n;
@@ -143,6 +149,9 @@ __global__ void __launch_bounds__(kThreads)
                const double* __restrict__ frames, const DetDev det,
                const GT* __restrict__ grad_img, OT* __restrict__ img,
                double* __restrict__ partials) {
+  extern __shared__ double tab[];
+  build_plane_table(g, tab);
+  __syncthreads();
   int h, w;
   tile_pixel(h, w);
   const int b = blockIdx.z;
@@ -159,7 +168,7 @@ __global__ void __launch_bounds__(kThreads)
     double e = 0.0;
     if (r.hit) {
       GradVisitor vis;
-      walk<VT, true>(vol, g, r, vis);
+      walk<VT>(vol, g, tab, r, vis);
       const double L = ray_length(r);
       e = L * vis.acc;
       double dEds[3], dEdp[3];
@@ -240,6 +249,9 @@ __global__ void __launch_bounds__(kRayThreads)
     k_raysum(const VT* __restrict__ vol, const GridDev g,
              const double* __restrict__ src, const double* __restrict__ pix,
              int64_t n_rays, double* __restrict__ out) {
+  extern __shared__ double tab[];
+  build_plane_table(g, tab);
+  __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_rays) return;
   double s[3] = {__ldg(src), __ldg(src + 1), __ldg(src + 2)};
@@ -249,7 +261,7 @@ __global__ void __launch_bounds__(kRayThreads)
   double e = 0.0;
   if (r.hit) {
     SumVisitor vis;
-    walk<VT, false>(vol, g, r, vis);
+    walk<VT>(vol, g, tab, r, vis);
     e = ray_length(r) * vis.acc;
   }
   out[i] = e;
@@ -262,6 +274,9 @@ __global__ void __launch_bounds__(kRayThreads)
                   const double* __restrict__ pix, int64_t n_rays,
                   double* __restrict__ out, double* __restrict__ dEds,
                   double* __restrict__ dEdp) {
+  extern __shared__ double tab[];
+  build_plane_table(g, tab);
+  __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_rays) return;
   double s[3] = {__ldg(src), __ldg(src + 1), __ldg(src + 2)};
@@ -271,7 +286,7 @@ __global__ void __launch_bounds__(kRayThreads)
   double e = 0.0, gs[3] = {0.0, 0.0, 0.0}, gp[3] = {0.0, 0.0, 0.0};
   if (r.hit) {
     GradVisitor vis;
-    walk<VT, true>(vol, g, r, vis);
+    walk<VT>(vol, g, tab, r, vis);
     const double L = ray_length(r);
     e = L * vis.acc;
     endpoint_grads(r, vis, L, gs, gp);
@@ -306,6 +321,18 @@ int check_launch(const char* what) {
   return DRR_OK;
 }
 
+// Dynamic shared memory for the per-CTA plane table; >48 KB needs opt-in.
+size_t table_bytes(const drr::GridDev& g) {
+  return static_cast<size_t>(drr::plane_table_len(g)) * sizeof(double);
+}
+
+template <typename Kernel>
+void ensure_smem(Kernel kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(bytes));
+}
+
 int make_grid(const drr_grid* in, drr::GridDev& g) {
   if (in == nullptr) return fail(DRR_ERR_INVALID_ARGUMENT, "grid is NULL");
   int64_t total = 1;
@@ -336,6 +363,9 @@ int make_grid(const drr_grid* in, drr::GridDev& g) {
   g.stride[1] = g.n[0];
   g.stride[2] = g.n[0] * g.n[1];
   g.total = static_cast<int>(total);
+  if (table_bytes(g) > 227 * 1024)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "plane table of %zu bytes exceeds shared memory",
+                table_bytes(g));
   return DRR_OK;
 }
 
@@ -366,13 +396,18 @@ void launch_backward(const VT* vol, const drr::GridDev& g,
                             const double* frames, const drr::DetDev& d,
                             int n_poses, const GT* grad, void* img,
                             int img_dtype, double* partials, cudaStream_t st) {
+  const size_t smem = table_bytes(g);
   const dim3 grd = pose_grid(d, n_poses);
-  if (img_dtype == 1)
-    drr::k_backward<VT, GT, double><<<grd, drr::kThreads, 0, st>>>(
+  if (img_dtype == 1) {
+    ensure_smem(drr::k_backward<VT, GT, double>, smem);
+    drr::k_backward<VT, GT, double><<<grd, drr::kThreads, smem, st>>>(
         vol, g, frames, d, grad, static_cast<double*>(img), partials);
-  else
-    drr::k_backward<VT, GT, float><<<grd, drr::kThreads, 0, st>>>(
+  }
+  else {
+    ensure_smem(drr::k_backward<VT, GT, float>, smem);
+    drr::k_backward<VT, GT, float><<<grd, drr::kThreads, smem, st>>>(
         vol, g, frames, d, grad, static_cast<float*>(img), partials);
+  }
 }
 
 }  // namespace
@@ -389,16 +424,21 @@ int drr_raysum(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::GridDev g;
   int rc = make_grid(grid, g);
   if (rc) return rc;
+  const size_t smem = table_bytes(g);
   if (n_rays < 0) return fail(DRR_ERR_INVALID_ARGUMENT, "n_rays < 0");
   if (n_rays == 0) return DRR_OK;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   const unsigned blocks = static_cast<unsigned>((n_rays + drr::kRayThreads - 1) / drr::kRayThreads);
-  if (vol_dtype == DRR_VOL_F32)
-    drr::k_raysum<float><<<blocks, drr::kRayThreads, 0, st>>>(
+  if (vol_dtype == DRR_VOL_F32) {
+    ensure_smem(drr::k_raysum<float>, smem);
+    drr::k_raysum<float><<<blocks, drr::kRayThreads, smem, st>>>(
         static_cast<const float*>(d_vol), g, d_src, d_pix, n_rays, d_out);
-  else if (vol_dtype == DRR_VOL_F64)
-    drr::k_raysum<double><<<blocks, drr::kRayThreads, 0, st>>>(
+  }
+  else if (vol_dtype == DRR_VOL_F64) {
+    ensure_smem(drr::k_raysum<double>, smem);
+    drr::k_raysum<double><<<blocks, drr::kRayThreads, smem, st>>>(
         static_cast<const double*>(d_vol), g, d_src, d_pix, n_rays, d_out);
+  }
   else
     return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
   return check_launch("drr_raysum");
@@ -412,16 +452,21 @@ int drr_raysum_endpoint_grad(const void* d_vol, int vol_dtype,
   drr::GridDev g;
   int rc = make_grid(grid, g);
   if (rc) return rc;
+  const size_t smem = table_bytes(g);
   if (n_rays < 0) return fail(DRR_ERR_INVALID_ARGUMENT, "n_rays < 0");
   if (n_rays == 0) return DRR_OK;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   const unsigned blocks = static_cast<unsigned>((n_rays + drr::kRayThreads - 1) / drr::kRayThreads);
-  if (vol_dtype == DRR_VOL_F32)
-    drr::k_raysum_grad<float><<<blocks, drr::kRayThreads, 0, st>>>(
+  if (vol_dtype == DRR_VOL_F32) {
+    ensure_smem(drr::k_raysum_grad<float>, smem);
+    drr::k_raysum_grad<float><<<blocks, drr::kRayThreads, smem, st>>>(
         static_cast<const float*>(d_vol), g, d_src, d_pix, n_rays, d_out, d_dEds, d_dEdp);
-  else if (vol_dtype == DRR_VOL_F64)
-    drr::k_raysum_grad<double><<<blocks, drr::kRayThreads, 0, st>>>(
+  }
+  else if (vol_dtype == DRR_VOL_F64) {
+    ensure_smem(drr::k_raysum_grad<double>, smem);
+    drr::k_raysum_grad<double><<<blocks, drr::kRayThreads, smem, st>>>(
         static_cast<const double*>(d_vol), g, d_src, d_pix, n_rays, d_out, d_dEds, d_dEdp);
+  }
   else
     return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
   return check_launch("drr_raysum_endpoint_grad");
@@ -435,6 +480,7 @@ int drr_forward(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::DetDev d;
   int rc = make_grid(grid, g);
   if (rc) return rc;
+  const size_t smem = table_bytes(g);
   rc = make_det(det, d);
   if (rc) return rc;
   if (n_poses < 0 || n_poses > 65535)
@@ -442,18 +488,26 @@ int drr_forward(const void* d_vol, int vol_dtype, const drr_grid* grid,
   if (n_poses == 0) return DRR_OK;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   const dim3 grd = pose_grid(d, n_poses);
-  if (vol_dtype == DRR_VOL_F32 && img_dtype == 0)
-    drr::k_forward<float, float><<<grd, drr::kThreads, 0, st>>>(
+  if (vol_dtype == DRR_VOL_F32 && img_dtype == 0) {
+    ensure_smem(drr::k_forward<float, float>, smem);
+    drr::k_forward<float, float><<<grd, drr::kThreads, smem, st>>>(
         static_cast<const float*>(d_vol), g, d_frames, d, static_cast<float*>(d_img));
-  else if (vol_dtype == DRR_VOL_F32 && img_dtype == 1)
-    drr::k_forward<float, double><<<grd, drr::kThreads, 0, st>>>(
+  }
+  else if (vol_dtype == DRR_VOL_F32 && img_dtype == 1) {
+    ensure_smem(drr::k_forward<float, double>, smem);
+    drr::k_forward<float, double><<<grd, drr::kThreads, smem, st>>>(
         static_cast<const float*>(d_vol), g, d_frames, d, static_cast<double*>(d_img));
-  else if (vol_dtype == DRR_VOL_F64 && img_dtype == 1)
-    drr::k_forward<double, double><<<grd, drr::kThreads, 0, st>>>(
+  }
+  else if (vol_dtype == DRR_VOL_F64 && img_dtype == 1) {
+    ensure_smem(drr::k_forward<double, double>, smem);
+    drr::k_forward<double, double><<<grd, drr::kThreads, smem, st>>>(
         static_cast<const double*>(d_vol), g, d_frames, d, static_cast<double*>(d_img));
-  else if (vol_dtype == DRR_VOL_F64 && img_dtype == 0)
-    drr::k_forward<double, float><<<grd, drr::kThreads, 0, st>>>(
+  }
+  else if (vol_dtype == DRR_VOL_F64 && img_dtype == 0) {
+    ensure_smem(drr::k_forward<double, float>, smem);
+    drr::k_forward<double, float><<<grd, drr::kThreads, smem, st>>>(
         static_cast<const double*>(d_vol), g, d_frames, d, static_cast<float*>(d_img));
+  }
   else
     return fail(DRR_ERR_INVALID_ARGUMENT, "bad dtypes vol=%d img=%d", vol_dtype, img_dtype);
   return check_launch("drr_forward");
@@ -476,6 +530,7 @@ int drr_backward(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::DetDev d;
   int rc = make_grid(grid, g);
   if (rc) return rc;
+  const size_t smem = table_bytes(g);
   rc = make_det(det, d);
   if (rc) return rc;
   if (n_poses < 0 || n_poses > 65535)
@@ -518,6 +573,7 @@ int drr_count_steps(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::DetDev d;
   int rc = make_grid(grid, g);
   if (rc) return rc;
+  const size_t smem = table_bytes(g);
   rc = make_det(det, d);
   if (rc) return rc;
   if (n_poses < 0 || n_poses > 65535)
@@ -525,12 +581,16 @@ int drr_count_steps(const void* d_vol, int vol_dtype, const drr_grid* grid,
   if (n_poses == 0) return DRR_OK;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   const dim3 grd = pose_grid(d, n_poses);
-  if (vol_dtype == DRR_VOL_F32)
-    drr::k_count<float><<<grd, drr::kThreads, 0, st>>>(
+  if (vol_dtype == DRR_VOL_F32) {
+    ensure_smem(drr::k_count<float>, smem);
+    drr::k_count<float><<<grd, drr::kThreads, smem, st>>>(
         static_cast<const float*>(d_vol), g, d_frames, d, d_steps);
-  else if (vol_dtype == DRR_VOL_F64)
-    drr::k_count<double><<<grd, drr::kThreads, 0, st>>>(
+  }
+  else if (vol_dtype == DRR_VOL_F64) {
+    ensure_smem(drr::k_count<double>, smem);
+    drr::k_count<double><<<grd, drr::kThreads, smem, st>>>(
         static_cast<const double*>(d_vol), g, d_frames, d, d_steps);
+  }
   else
     return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
   return check_launch("drr_count_steps");

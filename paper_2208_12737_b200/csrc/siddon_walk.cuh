@@ -84,17 +84,49 @@ __device__ __forceinline__ int exact_voxel(const GridDev& g, double s0, double s
   return i + g.n[0] * (j + g.n[1] * k);
 }
 
+// ---- plane table ---------------------------------------------------------
+// Per CTA, shared memory holds every plane coordinate P_a(k) = o_a + k*sp_a
+// (the reference's expression, _native.pyx:105) for k = 0..n_a, bracketed by
+// sentinels at k = -1 and k = n_a + 1 whose crossing parameter is a huge
+// positive number in the walking direction, so an exhausted axis simply never
+// wins the merge.  Axis a's P_a(0) sits at index plane_base(g, a).
+constexpr double kSentinel = 1e280;
+
+__host__ __device__ __forceinline__ int plane_table_len(const GridDev& g) {
+  return g.n[0] + g.n[1] + g.n[2] + 9;
+}
+__host__ __device__ __forceinline__ int plane_base(const GridDev& g, int a) {
+  return a == 0 ? 1 : (a == 1 ? g.n[0] + 4 : g.n[0] + g.n[1] + 7);
+}
+
+__device__ __forceinline__ void build_plane_table(const GridDev& g, double* tab) {
+  const int l0 = g.n[0] + 3, l1 = g.n[1] + 3, l2 = g.n[2] + 3;
+  for (int i = threadIdx.x; i < l0 + l1 + l2; i += blockDim.x) {
+    int j, n;
+    double o, sp;
+    if (i < l0) { j = i; n = g.n[0]; o = g.o[0]; sp = g.sp[0]; }
+    else if (i < l0 + l1) { j = i - l0; n = g.n[1]; o = g.o[1]; sp = g.sp[1]; }
+    else { j = i - l0 - l1; n = g.n[2]; o = g.o[2]; sp = g.sp[2]; }
+    const int k = j - 1;
+    double v;
+    if (k < 0) v = -kSentinel;
+    else if (k > n) v = kSentinel;
+    else v = o + static_cast<double>(k) * sp;
+    tab[i] = v;
+  }
+}
+
 struct Ray {
   double s[3], d[3], inv[3];
-  double an[3];     // crossing parameter of the next plane per axis (+inf: none)
-  int kn[3];        // index of the next plane per axis
+  double an[3];     // crossing parameter of the next plane per axis
+  int q[3];         // plane-table index of that plane
   int st[3];        // +1 / -1 walking direction, 0 for a parallel axis
   double amin, amax;
   double T;         // fast-voxel threshold on seg (see ray_setup)
   int lab_min, lab_max;
-  int flat;         // flat voxel index of the segment after `prev`
+  int flat;         // flat voxel index of the segment after amin
   bool hit;
-  bool safe;        // some |d_a| so small that RN(1/d_a) overflows: use IEEE '/'
+  bool safe;        // some |d_a| tiny: use IEEE '/' instead of the Markstein form
 };
 
 // Slab entry/exit, first-max/first-min labels over (x, y, z, clip):
@@ -154,7 +186,7 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
       // Constant index along a parallel axis: the reference evaluates
       // floor(((s + mid*0) - o)/sp) = floor((s - o)/sp), then clamps.
       r.st[a] = 0;
-      r.kn[a] = 0;
+      r.q[a] = plane_base(g, a);
       r.inv[a] = 0.0;
       r.an[a] = INFINITY;
       const double f = floor((r.s[a] - g.o[a]) / g.sp[a]);
@@ -162,7 +194,7 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
       continue;
     }
     const double inv = __drcp_rn(d);
-    if (!(fabs(inv) < 1e300)) r.safe = true;
+    if (!(fabs(d) > 1e-20)) r.safe = true;
     const int st = d > 0.0 ? 1 : -1;
     r.inv[a] = inv;
     r.st[a] = st;
@@ -187,10 +219,10 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
       }
       break;
     }
-    r.kn[a] = k;
+    r.q[a] = plane_base(g, a) + k;
     r.an[a] = (k >= 0 && k <= n)
                   ? plane_alpha(g.o[a], g.sp[a], k, r.s[a], d, inv, true)
-                  : INFINITY;
+                  : kSentinel;
     vox[a] = st > 0 ? k - 1 : k;
     // Fast-voxel certificate.  The reference's midpoint position and our
     // crossing parameters carry rounding error below ~2^-50 * M voxels, with
@@ -206,103 +238,107 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
   r.flat = vox[0] + g.stride[1] * vox[1] + g.stride[2] * vox[2];
 }
 
-// Walks the ray, calling `on_segment(v, seg, prev, cur, lab_prev, lab_cur)`
-// for every used segment in ascending order and `on_crossing` bookkeeping in
-// the visitor.  Returns the raw sum acc (E = |d| * acc).
-//
-// Visitor interface:
-//   vis.segment(double v, double seg)        -- used segment, value v
-//   vis.crossing(int label, double alpha, double v_after)
-//       -- called once per crossing (entry first, exit last) with the value of
-//          the used segment that STARTS at it (0 when skipped); the visitor
-//          derives the crossing's reverse-mode coefficient from it.
-template <typename VT, bool kCrossings, typename Visitor>
+// The walk.  Visits every segment between consecutive crossings in ascending
+// order (ties -> lowest axis), calling
+//   vis.segment(used, seg, v, lab_start, alpha_start)
+// for each (v = V[voxel] for used segments), then vis.finish(lab_max, amax).
+// Branch-free axis selection: the crossed axis's constants are picked with
+// selects, so lanes taking different axes never diverge.  The gather of
+// segment i is consumed in iteration i+1 (one-deep software pipeline) so its
+// latency overlaps the next crossing's arithmetic.
+template <typename VT, typename Visitor>
 __device__ __forceinline__ void walk(const VT* __restrict__ vol,
-                                     const GridDev& g, Ray& r, Visitor& vis) {
+                                     const GridDev& g,
+                                     const double* __restrict__ tab,
+                                     const Ray& r, Visitor& vis) {
   double an0 = r.an[0], an1 = r.an[1], an2 = r.an[2];
-  int k0 = r.kn[0], k1 = r.kn[1], k2 = r.kn[2];
+  int q0 = r.q[0], q1 = r.q[1], q2 = r.q[2];
+  const double s0 = r.s[0], s1 = r.s[1], s2 = r.s[2];
+  const double d0 = r.d[0], d1 = r.d[1], d2 = r.d[2];
+  const double i0 = r.inv[0], i1 = r.inv[1], i2 = r.inv[2];
+  const int st0 = r.st[0], st1 = r.st[1], st2 = r.st[2];
+  const int df0 = st0, df1 = st1 * g.stride[1], df2 = st2 * g.stride[2];
+  const double amax = r.amax, T = r.T;
+  const bool safe = r.safe;
+  const unsigned total = static_cast<unsigned>(g.total);
   int flat = r.flat;
   double prev = r.amin;
-  int lab_prev = r.lab_min;
-  const int total = g.total;
+  int lab = r.lab_min;
+  bool p_used = false;
+  double p_seg = 0.0, p_a = 0.0;
+  int p_lab = 0;
+  VT p_v = VT(0);
   for (;;) {
-    double best = an0;
-    int sel = 0;
-    if (an1 < best) { best = an1; sel = 1; }
-    if (an2 < best) { best = an2; sel = 2; }
-    const bool last = !(best <= r.amax);
-    const double cur = last ? r.amax : best;
+    const bool c1 = an1 < an0;
+    double best = c1 ? an1 : an0;
+    const bool c2 = an2 < best;
+    best = c2 ? an2 : best;
+    const bool last = !(best <= amax);
+    const double cur = last ? amax : best;
     const double seg = cur - prev;
-    double v = 0.0;
-    if (seg > kSegEps) {
-      int idx = flat;
-      if (!(seg > r.T) || static_cast<unsigned>(flat) >= static_cast<unsigned>(total))
-        idx = exact_voxel(g, r.s[0], r.s[1], r.s[2], r.d[0], r.d[1], r.d[2],
-                          0.5 * (prev + cur));
-      v = load_voxel(vol, idx);
-      vis.segment(v, seg);
-    }
-    if (kCrossings) vis.crossing(lab_prev, prev, v);
+    const bool used = seg > kSegEps;
+    int idx = flat;
+    if (used && (!(seg > T) || static_cast<unsigned>(flat) >= total))
+      idx = exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
+    VT v = VT(0);
+    if (used) v = __ldg(vol + idx);
+    vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
+    p_used = used;
+    p_seg = seg;
+    p_v = v;
+    p_lab = lab;
+    p_a = prev;
     prev = cur;
-    if (last) {
-      if (kCrossings) vis.crossing(r.lab_max, cur, 0.0);
-      break;
-    }
-    lab_prev = sel;
-    // Advance the selected axis to its next plane.
-    double o, sp, s, d, inv;
-    int k, st, n, df;
-    if (sel == 0) {
-      o = g.o[0]; sp = g.sp[0]; s = r.s[0]; d = r.d[0]; inv = r.inv[0];
-      k = k0; st = r.st[0]; n = g.n[0]; df = st;
-    } else if (sel == 1) {
-      o = g.o[1]; sp = g.sp[1]; s = r.s[1]; d = r.d[1]; inv = r.inv[1];
-      k = k1; st = r.st[1]; n = g.n[1]; df = st * g.stride[1];
-    } else {
-      o = g.o[2]; sp = g.sp[2]; s = r.s[2]; d = r.d[2]; inv = r.inv[2];
-      k = k2; st = r.st[2]; n = g.n[2]; df = st * g.stride[2];
-    }
-    k += st;
-    const double anew =
-        (k >= 0 && k <= n) ? plane_alpha(o, sp, k, s, d, inv, r.safe) : INFINITY;
-    flat += df;
-    if (sel == 0) { an0 = anew; k0 = k; }
-    else if (sel == 1) { an1 = anew; k1 = k; }
-    else { an2 = anew; k2 = k; }
+    if (last) break;
+    const double s = c2 ? s2 : (c1 ? s1 : s0);
+    const double d = c2 ? d2 : (c1 ? d1 : d0);
+    const double inv = c2 ? i2 : (c1 ? i1 : i0);
+    const int q = (c2 ? q2 : (c1 ? q1 : q0)) + (c2 ? st2 : (c1 ? st1 : st0));
+    const double num = tab[q] - s;
+    const double an = safe ? num / d : div_rn(num, d, inv);
+    const bool a0 = !(c1 || c2), a1 = c1 && !c2;
+    an0 = a0 ? an : an0;
+    an1 = a1 ? an : an1;
+    an2 = c2 ? an : an2;
+    q0 = a0 ? q : q0;
+    q1 = a1 ? q : q1;
+    q2 = c2 ? q : q2;
+    flat += c2 ? df2 : (c1 ? df1 : df0);
+    lab = c2 ? 2 : (c1 ? 1 : 0);
   }
+  vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
+  vis.finish(r.lab_max, amax);
 }
 
 // ---- visitors ----------------------------------------------------------
 
 struct SumVisitor {
   double acc = 0.0;
-  __device__ __forceinline__ void segment(double v, double seg) {
-    acc = acc + seg * v;  // _native.pyx:187, no FMA (TU built --fmad=false)
+  __device__ __forceinline__ void segment(bool used, double seg, double v, int,
+                                          double) {
+    if (used) acc = acc + seg * v;  // _native.pyx:187 (TU built --fmad=false)
   }
-  __device__ __forceinline__ void crossing(int, double, double) {}
+  __device__ __forceinline__ void finish(int, double) {}
 };
 
 struct CountVisitor {
   int steps = 0;
-  __device__ __forceinline__ void segment(double, double) { ++steps; }
-  __device__ __forceinline__ void crossing(int, double, double) {}
+  __device__ __forceinline__ void segment(bool used, double, double, int, double) {
+    steps += used ? 1 : 0;
+  }
+  __device__ __forceinline__ void finish(int, double) {}
 };
 
 // Reverse mode: each crossing k on axis a carries the coefficient
-// c_k = v(segment ending at k) - v(segment starting at k); with
-// d alpha_k/ds_a = (alpha_k - 1)/d_a and d alpha_k/dp_a = -alpha_k/d_a the ray's
-// endpoint gradients need only G_a = sum c_k and H_a = sum c_k alpha_k.
+// c_k = v(segment ending at k) - v(segment starting at k) (0 for skipped
+// segments); with d alpha_k/ds_a = (alpha_k - 1)/d_a and
+// d alpha_k/dp_a = -alpha_k/d_a the ray's endpoint gradients need only
+// G_a = sum c_k and H_a = sum c_k alpha_k.  Label 3 (clip) has no tangent.
 struct GradVisitor {
   double acc = 0.0;
   double pend = 0.0;  // value of the used segment ending at the next crossing
   double G0 = 0.0, G1 = 0.0, G2 = 0.0, H0 = 0.0, H1 = 0.0, H2 = 0.0;
-  __device__ __forceinline__ void segment(double v, double seg) {
-    acc = acc + seg * v;
-  }
-  __device__ __forceinline__ void crossing(int label, double alpha,
-                                           double v_after) {
-    const double c = pend - v_after;
-    pend = v_after;
+  __device__ __forceinline__ void apply(int label, double alpha, double c) {
     const double c0 = label == 0 ? c : 0.0;
     const double c1 = label == 1 ? c : 0.0;
     const double c2 = label == 2 ? c : 0.0;
@@ -310,6 +346,16 @@ struct GradVisitor {
     H0 = __fma_rn(c0, alpha, H0);
     H1 = __fma_rn(c1, alpha, H1);
     H2 = __fma_rn(c2, alpha, H2);
+  }
+  __device__ __forceinline__ void segment(bool used, double seg, double v,
+                                          int lab_start, double a_start) {
+    const double vv = used ? v : 0.0;
+    if (used) acc = acc + seg * v;
+    apply(lab_start, a_start, pend - vv);
+    pend = vv;
+  }
+  __device__ __forceinline__ void finish(int lab_end, double a_end) {
+    apply(lab_end, a_end, pend);
   }
 };
 
