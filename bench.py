@@ -47,7 +47,7 @@ WORKLOAD = ("C2: synthetic chest CT 512x512x133 @ (0.703125,0.703125,2.5) mm fp3
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--batch", type=int, default=32, help="poses per GPU per step")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -72,8 +72,9 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.5)  # nvidia-smi start-up: sample before the timed region begins
         except OSError:
             self.proc = None
         return self
@@ -384,7 +385,12 @@ def main():
         vol_np = vol_np if vol_np is not None else synthetic.chest_phantom(DIMS)
         kind, worker, fixed_np = cpu_setup(vol_np)
         procs = os.cpu_count() or 1
-        n = args.cpu_sample or procs
+        if args.cpu_sample:
+            n = args.cpu_sample
+        else:  # size the sample to ~15 s of wall time on this host
+            t1, _ = cpu_run(worker, synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS,
+                                                           procs, seed=2), fixed_np, procs)
+            n = procs * max(1, min(64, int(15.0 / max(t1, 1e-3))))
         poses = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, n, seed=1)
         wall, res = cpu_run(worker, poses, fixed_np, procs)
         result["cpu_baseline"] = {
