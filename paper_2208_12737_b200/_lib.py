@@ -13,7 +13,8 @@ import os
 
 from .errors import GradientUndefinedError, InvalidArgumentError, KernelError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libdrr_b200.so")
+LIB_PATH = os.environ.get("DRR_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libdrr_b200.so")
 
 DRR_OK = 0
 DRR_ERR_INVALID_ARGUMENT = -1

@@ -87,27 +87,31 @@ __device__ __forceinline__ int exact_voxel(const GridDev& g, double s0, double s
 // ---- plane table ---------------------------------------------------------
 // Per CTA, shared memory holds every plane coordinate P_a(k) = o_a + k*sp_a
 // (the reference's expression, _native.pyx:105) for k = 0..n_a, bracketed by
-// sentinels at k = -1 and k = n_a + 1 whose crossing parameter is a huge
-// positive number in the walking direction, so an exhausted axis simply never
-// wins the merge.  Axis a's P_a(0) sits at index plane_base(g, a).
+// kPad sentinel slots on each side whose crossing parameter is a huge positive
+// number in the walking direction, so an exhausted axis never wins the merge
+// (and the lookahead walk may read up to kPad slots past the last plane).
+// Axis a's P_a(0) sits at index plane_base(g, a).
 constexpr double kSentinel = 1e280;
+constexpr int kPad = 3;
 
 __host__ __device__ __forceinline__ int plane_table_len(const GridDev& g) {
-  return g.n[0] + g.n[1] + g.n[2] + 9;
+  return g.n[0] + g.n[1] + g.n[2] + 3 * (2 * kPad + 1);
 }
 __host__ __device__ __forceinline__ int plane_base(const GridDev& g, int a) {
-  return a == 0 ? 1 : (a == 1 ? g.n[0] + 4 : g.n[0] + g.n[1] + 7);
+  return a == 0 ? kPad
+                : (a == 1 ? g.n[0] + 1 + 3 * kPad : g.n[0] + g.n[1] + 2 + 5 * kPad);
 }
 
 __device__ __forceinline__ void build_plane_table(const GridDev& g, double* tab) {
-  const int l0 = g.n[0] + 3, l1 = g.n[1] + 3, l2 = g.n[2] + 3;
+  const int l0 = g.n[0] + 1 + 2 * kPad, l1 = g.n[1] + 1 + 2 * kPad,
+            l2 = g.n[2] + 1 + 2 * kPad;
   for (int i = threadIdx.x; i < l0 + l1 + l2; i += blockDim.x) {
     int j, n;
     double o, sp;
     if (i < l0) { j = i; n = g.n[0]; o = g.o[0]; sp = g.sp[0]; }
     else if (i < l0 + l1) { j = i - l0; n = g.n[1]; o = g.o[1]; sp = g.sp[1]; }
     else { j = i - l0 - l1; n = g.n[2]; o = g.o[2]; sp = g.sp[2]; }
-    const int k = j - 1;
+    const int k = j - kPad;
     double v;
     if (k < 0) v = -kSentinel;
     else if (k > n) v = kSentinel;
@@ -247,10 +251,10 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
 // segment i is consumed in iteration i+1 (one-deep software pipeline) so its
 // latency overlaps the next crossing's arithmetic.
 template <typename VT, typename Visitor>
-__device__ __forceinline__ void walk(const VT* __restrict__ vol,
-                                     const GridDev& g,
-                                     const double* __restrict__ tab,
-                                     const Ray& r, Visitor& vis) {
+__device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
+                                            const GridDev& g,
+                                            const double* __restrict__ tab,
+                                            const Ray& r, Visitor& vis) {
   double an0 = r.an[0], an1 = r.an[1], an2 = r.an[2];
   int q0 = r.q[0], q1 = r.q[1], q2 = r.q[2];
   const double s0 = r.s[0], s1 = r.s[1], s2 = r.s[2];
@@ -308,6 +312,96 @@ __device__ __forceinline__ void walk(const VT* __restrict__ vol,
   }
   vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
   vis.finish(r.lab_max, amax);
+}
+
+// Lookahead variant: every axis carries its next AND next-next crossing
+// parameter; each iteration speculatively computes the crossing after that for
+// all three axes (axis-specific registers, no selects of per-axis constants,
+// full ILP) and commits it only for the crossed axis.  The division is off the
+// loop-carried dependency chain (argmin -> commit).
+template <typename VT, typename Visitor>
+__device__ __forceinline__ void walk_lookahead(const VT* __restrict__ vol,
+                                               const GridDev& g,
+                                               const double* __restrict__ tab,
+                                               const Ray& r, Visitor& vis) {
+  const double s0 = r.s[0], s1 = r.s[1], s2 = r.s[2];
+  const double d0 = r.d[0], d1 = r.d[1], d2 = r.d[2];
+  const double i0 = r.inv[0], i1 = r.inv[1], i2 = r.inv[2];
+  const int st0 = r.st[0], st1 = r.st[1], st2 = r.st[2];
+  const int df0 = st0, df1 = st1 * g.stride[1], df2 = st2 * g.stride[2];
+  const double amax = r.amax, T = r.T;
+  const bool safe = r.safe;
+  const unsigned total = static_cast<unsigned>(g.total);
+  // q_a: table index of the plane AFTER the next one (the next-next plane).
+  int q0 = r.q[0] + st0, q1 = r.q[1] + st1, q2 = r.q[2] + st2;
+  auto alpha = [&](int q, double s, double d, double inv) {
+    const double num = tab[q] - s;
+    return safe ? num / d : div_rn(num, d, inv);
+  };
+  double an0 = r.an[0], an1 = r.an[1], an2 = r.an[2];
+  // parallel axes keep +inf; their q stays parked on P(0) (never read past)
+  double nn0 = st0 ? alpha(q0, s0, d0, i0) : INFINITY;
+  double nn1 = st1 ? alpha(q1, s1, d1, i1) : INFINITY;
+  double nn2 = st2 ? alpha(q2, s2, d2, i2) : INFINITY;
+  // an exhausted axis (next plane is a sentinel) must not read beyond the table
+  if (!(an0 < kSentinel)) { nn0 = kSentinel; q0 -= st0; }
+  if (!(an1 < kSentinel)) { nn1 = kSentinel; q1 -= st1; }
+  if (!(an2 < kSentinel)) { nn2 = kSentinel; q2 -= st2; }
+  int flat = r.flat;
+  double prev = r.amin;
+  int lab = r.lab_min;
+  bool p_used = false;
+  double p_seg = 0.0, p_a = 0.0;
+  int p_lab = 0;
+  VT p_v = VT(0);
+  for (;;) {
+    const bool c1 = an1 < an0;
+    const bool c2 = (an2 < an0) && (an2 < an1);
+    const double best = c2 ? an2 : (c1 ? an1 : an0);
+    const bool last = !(best <= amax);
+    const double cur = last ? amax : best;
+    const double seg = cur - prev;
+    const bool used = seg > kSegEps;
+    int idx = flat;
+    if (used && (!(seg > T) || static_cast<unsigned>(flat) >= total))
+      idx = exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
+    VT v = VT(0);
+    if (used) v = __ldg(vol + idx);
+    vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
+    p_used = used;
+    p_seg = seg;
+    p_v = v;
+    p_lab = lab;
+    p_a = prev;
+    prev = cur;
+    if (last) break;
+    // speculative next-next-next crossings (sentinel slots clamp the index)
+    const int n0 = q0 + st0, n1 = q1 + st1, n2 = q2 + st2;
+    const double x0 = alpha(n0, s0, d0, i0);
+    const double x1 = alpha(n1, s1, d1, i1);
+    const double x2 = alpha(n2, s2, d2, i2);
+    const bool a0 = !(c1 || c2), a1 = c1 && !c2;
+    if (a0) { an0 = nn0; nn0 = x0; q0 = n0; flat += df0; }
+    if (a1) { an1 = nn1; nn1 = x1; q1 = n1; flat += df1; }
+    if (c2) { an2 = nn2; nn2 = x2; q2 = n2; flat += df2; }
+    lab = c2 ? 2 : (c1 ? 1 : 0);
+  }
+  vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
+  vis.finish(r.lab_max, amax);
+}
+
+#ifndef DRR_WALK
+#define DRR_WALK 3
+#endif
+template <typename VT, typename Visitor>
+__device__ __forceinline__ void walk(const VT* __restrict__ vol, const GridDev& g,
+                                     const double* __restrict__ tab, const Ray& r,
+                                     Visitor& vis) {
+#if DRR_WALK == 3
+  walk_lookahead<VT>(vol, g, tab, r, vis);
+#else
+  walk_select<VT>(vol, g, tab, r, vis);
+#endif
 }
 
 // ---- visitors ----------------------------------------------------------
