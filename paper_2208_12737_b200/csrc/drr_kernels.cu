@@ -26,6 +26,16 @@
 
 namespace drr {
 
+// Occupancy knob for experiments: DRR_MINB=n adds a minimum-blocks-per-SM
+// launch bound (0 = let ptxas choose).
+#ifndef DRR_MINB
+#define DRR_MINB 0
+#endif
+#if DRR_MINB > 0
+#define DRR_LB __launch_bounds__(kThreads, DRR_MINB)
+#else
+#define DRR_LB __launch_bounds__(kThreads)
+#endif
 constexpr int kTileW = 16;
 constexpr int kTileH = 8;
 constexpr int kThreads = kTileW * kTileH;  // 4 warps, each an 8 x 4 quad
@@ -73,7 +83,7 @@ __device__ __forceinline__ void store_out(OT* p, double v) {
 
 // ---------------------------------------------------------------- forward
 template <typename VT, typename OT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void DRR_LB
     k_forward(const VT* __restrict__ vol, const GridDev g,
               const double* __restrict__ frames, const DetDev det,
               OT* __restrict__ img) {
@@ -91,14 +101,14 @@ __global__ void __launch_bounds__(kThreads)
   double e = 0.0;
   if (r.hit) {
     SumVisitor vis;
-    walk<VT>(vol, g, tab, r, vis);
+    walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
     e = ray_length(r) * vis.acc;
   }
   store_out(img + (static_cast<size_t>(b) * det.H + h) * det.W + w, e);
 }
 
 template <typename VT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void DRR_LB
     k_count(const VT* __restrict__ vol, const GridDev g,
             const double* __restrict__ frames, const DetDev det,
             int* __restrict__ steps) {
@@ -116,7 +126,7 @@ __global__ void __launch_bounds__(kThreads)
   int n = 0;
   if (r.hit) {
     CountVisitor vis;
-    walk<VT>(vol, g, tab, r, vis);
+    walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
     n = vis.steps;
   }
   steps[(static_cast<size_t>(b) * det.H + h) * det.W + w] = n;
@@ -144,7 +154,7 @@ __device__ __forceinline__ void endpoint_grads(const Ray& r,
 
 // --------------------------------------------------------------- backward
 template <typename VT, typename GT, typename OT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void DRR_LB
     k_backward(const VT* __restrict__ vol, const GridDev g,
                const double* __restrict__ frames, const DetDev det,
                const GT* __restrict__ grad_img, OT* __restrict__ img,
@@ -168,7 +178,7 @@ __global__ void __launch_bounds__(kThreads)
     double e = 0.0;
     if (r.hit) {
       GradVisitor vis;
-      walk<VT>(vol, g, tab, r, vis);
+      walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
       const double L = ray_length(r);
       e = L * vis.acc;
       double dEds[3], dEdp[3];
@@ -261,7 +271,7 @@ __global__ void __launch_bounds__(kRayThreads)
   double e = 0.0;
   if (r.hit) {
     SumVisitor vis;
-    walk<VT>(vol, g, tab, r, vis);
+    walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
     e = ray_length(r) * vis.acc;
   }
   out[i] = e;
@@ -286,7 +296,7 @@ __global__ void __launch_bounds__(kRayThreads)
   double e = 0.0, gs[3] = {0.0, 0.0, 0.0}, gp[3] = {0.0, 0.0, 0.0};
   if (r.hit) {
     GradVisitor vis;
-    walk<VT>(vol, g, tab, r, vis);
+    walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
     const double L = ray_length(r);
     e = L * vis.acc;
     endpoint_grads(r, vis, L, gs, gp);
@@ -323,7 +333,9 @@ int check_launch(const char* what) {
 
 // Dynamic shared memory for the per-CTA plane table; >48 KB needs opt-in.
 size_t table_bytes(const drr::GridDev& g) {
-  return static_cast<size_t>(drr::plane_table_len(g)) * sizeof(double);
+  // plane table + the walk's per-thread constants (both kernels use <= 128 threads)
+  return (static_cast<size_t>(drr::plane_table_len(g)) +
+          static_cast<size_t>(drr::kWalkSmemDoublesPerThread) * 128) * sizeof(double);
 }
 
 template <typename Kernel>

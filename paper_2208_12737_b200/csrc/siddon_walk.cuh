@@ -390,15 +390,101 @@ __device__ __forceinline__ void walk_lookahead(const VT* __restrict__ vol,
   vis.finish(r.lab_max, amax);
 }
 
+// Shared-memory-constant variant: each thread parks its per-axis ray
+// constants (s_a, d_a, 1/d_a, walking step) in shared memory, field-major
+// ([field][axis][thread]) so a warp's loads are conflict-free whichever axis
+// each lane crosses; the crossed axis's constants are then 3 LDS.64 + 1 LDS.64
+// instead of 16 ALU selects.  `cst` points at this CTA's block of 4*3*blockDim
+// doubles.
+template <typename VT, typename Visitor>
+__device__ __forceinline__ void walk_smem(const VT* __restrict__ vol,
+                                          const GridDev& g,
+                                          const double* __restrict__ tab,
+                                          double* __restrict__ cst,
+                                          const Ray& r, Visitor& vis) {
+  const int nt = blockDim.x, t = threadIdx.x;
+  double* cs = cst + t;               // s  : cs[a*nt]
+  double* cd = cst + 3 * nt + t;      // d  : cd[a*nt]
+  double* ci = cst + 6 * nt + t;      // inv: ci[a*nt]
+  int2* cx = reinterpret_cast<int2*>(cst + 9 * nt) + t;  // (st, dflat)
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cs[a * nt] = r.s[a];
+    cd[a * nt] = r.d[a];
+    ci[a * nt] = r.inv[a];
+    cx[a * nt] = make_int2(r.st[a], r.st[a] * g.stride[a]);
+  }
+  double an0 = r.an[0], an1 = r.an[1], an2 = r.an[2];
+  int q0 = r.q[0], q1 = r.q[1], q2 = r.q[2];
+  const double amax = r.amax, T = r.T;
+  const bool safe = r.safe;
+  const unsigned total = static_cast<unsigned>(g.total);
+  int flat = r.flat;
+  double prev = r.amin;
+  int lab = r.lab_min;
+  bool p_used = false;
+  double p_seg = 0.0, p_a = 0.0;
+  int p_lab = 0;
+  VT p_v = VT(0);
+  for (;;) {
+    const bool c1 = an1 < an0;
+    double best = c1 ? an1 : an0;
+    const bool c2 = an2 < best;
+    best = c2 ? an2 : best;
+    const bool last = !(best <= amax);
+    const double cur = last ? amax : best;
+    const double seg = cur - prev;
+    const bool used = seg > kSegEps;
+    int idx = flat;
+    if (used && (!(seg > T) || static_cast<unsigned>(flat) >= total))
+      idx = exact_voxel(g, r.s[0], r.s[1], r.s[2], r.d[0], r.d[1], r.d[2],
+                        0.5 * (prev + cur));
+    VT v = VT(0);
+    if (used) v = __ldg(vol + idx);
+    vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
+    p_used = used;
+    p_seg = seg;
+    p_v = v;
+    p_lab = lab;
+    p_a = prev;
+    prev = cur;
+    if (last) break;
+    const int sel = c2 ? 2 : (c1 ? 1 : 0);
+    const int o = sel * nt;
+    const double s = cs[o], d = cd[o], inv = ci[o];
+    const int2 x = cx[o];
+    const int q = (c2 ? q2 : (c1 ? q1 : q0)) + x.x;
+    const double num = tab[q] - s;
+    const double an = safe ? num / d : div_rn(num, d, inv);
+    const bool a0 = !(c1 || c2), a1 = c1 && !c2;
+    an0 = a0 ? an : an0;
+    an1 = a1 ? an : an1;
+    an2 = c2 ? an : an2;
+    q0 = a0 ? q : q0;
+    q1 = a1 ? q : q1;
+    q2 = c2 ? q : q2;
+    flat += x.y;
+    lab = sel;
+  }
+  vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
+  vis.finish(r.lab_max, amax);
+}
+
 #ifndef DRR_WALK
-#define DRR_WALK 3
+#define DRR_WALK 2
 #endif
+// Per-thread shared-memory doubles the walk needs beyond the plane table.
+constexpr int kWalkSmemDoublesPerThread = (DRR_WALK == 4) ? 12 : 0;
+
 template <typename VT, typename Visitor>
 __device__ __forceinline__ void walk(const VT* __restrict__ vol, const GridDev& g,
-                                     const double* __restrict__ tab, const Ray& r,
+                                     const double* __restrict__ tab,
+                                     double* __restrict__ cst, const Ray& r,
                                      Visitor& vis) {
 #if DRR_WALK == 3
   walk_lookahead<VT>(vol, g, tab, r, vis);
+#elif DRR_WALK == 4
+  walk_smem<VT>(vol, g, tab, cst, r, vis);
 #else
   walk_select<VT>(vol, g, tab, r, vis);
 #endif
@@ -410,7 +496,10 @@ struct SumVisitor {
   double acc = 0.0;
   __device__ __forceinline__ void segment(bool used, double seg, double v, int,
                                           double) {
-    if (used) acc = acc + seg * v;  // _native.pyx:187 (TU built --fmad=false)
+    // _native.pyx:187 (TU built --fmad=false).  Unused segments arrive with
+    // v = 0 and seg >= 0, so adding seg*v = +0 leaves acc bit-identical.
+    (void)used;
+    acc = acc + seg * v;
   }
   __device__ __forceinline__ void finish(int, double) {}
 };
@@ -444,7 +533,7 @@ struct GradVisitor {
   __device__ __forceinline__ void segment(bool used, double seg, double v,
                                           int lab_start, double a_start) {
     const double vv = used ? v : 0.0;
-    if (used) acc = acc + seg * v;
+    acc = acc + seg * vv;
     apply(lab_start, a_start, pend - vv);
     pend = vv;
   }
