@@ -36,6 +36,12 @@ namespace drr {
 #else
 #define DRR_LB __launch_bounds__(kThreads)
 #endif
+// The backward re-walk carries 13 more live doubles than the forward; capping
+// it at <= 96 registers (5 CTAs/SM) measured faster than ptxas's 111
+// (profiles/r01_v2 A/B: 4.34 vs 4.93 ms for 32 C2 poses).
+#ifndef DRR_BWD_MINB
+#define DRR_BWD_MINB 5
+#endif
 constexpr int kTileW = 16;
 constexpr int kTileH = 8;
 constexpr int kThreads = kTileW * kTileH;  // 4 warps, each an 8 x 4 quad
@@ -154,7 +160,7 @@ __device__ __forceinline__ void endpoint_grads(const Ray& r,
 
 // --------------------------------------------------------------- backward
 template <typename VT, typename GT, typename OT>
-__global__ void DRR_LB
+__global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
     k_backward(const VT* __restrict__ vol, const GridDev g,
                const double* __restrict__ frames, const DetDev det,
                const GT* __restrict__ grad_img, OT* __restrict__ img,
