@@ -23,6 +23,15 @@
  *                               mode down to the 12-number frame (s, c, e1, e2)
  *   drr_count_steps          <- _kernels/python_ref.py:191-201 ray_structure
  *                               (number of used voxel-steps per ray)
+ *   drr_pose_frames          <- geometry.py:120-149 _pose_frame (+ the
+ *                               isocenter offset of geometry.py:166-175), batched
+ *   drr_pose_grad            <- the tangent half of the same map (dual.py
+ *                               duals seeded in geometry.py:130-131): dL/dframe
+ *                               -> dL/d(rho, theta, phi, gamma, bx, by, bz)
+ *   drr_image_loss           <- metrics.py:71-91 loss_value_and_pixel_grad
+ *                               (neg_zncc, l2), batched, fused
+ *   drr_register_update      <- one iteration of registration.py:89-125
+ *                               register() (momentum GD + convergence state)
  */
 #ifndef DRR_B200_H
 #define DRR_B200_H
@@ -105,6 +114,52 @@ int drr_backward(const void *d_vol, int vol_dtype, const drr_grid *grid,
 int drr_count_steps(const void *d_vol, int vol_dtype, const drr_grid *grid,
                     const double *d_frames, int32_t n_poses,
                     const drr_detector *det, int32_t *d_steps, void *stream);
+
+/* B x 7 pose vectors (rho, theta, phi, gamma, bx, by, bz) -> B x 12 frames.
+ * isocenter: 3 doubles in HOST memory (the volume centre). */
+int drr_pose_frames(const double *d_eta, int32_t n_poses,
+                    const double *isocenter, double *d_frames, void *stream);
+
+/* dL/dframe (B x 12) -> dL/deta (B x 7) at poses d_eta. */
+int drr_pose_grad(const double *d_eta, const double *d_grad_frames,
+                  int32_t n_poses, double *d_grad_eta, void *stream);
+
+#define DRR_LOSS_NEG_ZNCC 0
+#define DRR_LOSS_L2 1
+/* Per-image loss value (B doubles) and optional fp32 pixel gradient
+ * (B x npix) of img (B x npix) against fixed (fixed_stride = 0: one image
+ * shared by all; = npix: one per image).  img_dtype 0 = float32, 1 = float64
+ * (fixed has the same dtype).  d_status (optional, B ints) = 1 where the
+ * metric is undefined (zero variance, metrics.py:29-30). */
+int drr_image_loss(const void *d_img, const void *d_fixed, int img_dtype,
+                   int64_t fixed_stride, int32_t n_images, int64_t npix,
+                   int kind, double *d_value, float *d_grad, int *d_status,
+                   void *stream);
+
+/* Momentum gradient descent settings (registration.py:41-58). */
+typedef struct drr_reg_config {
+  double lr_rotation;
+  double lr_translation;
+  double momentum;
+  double converged_threshold;
+  int32_t max_iters;
+} drr_reg_config;
+
+#define DRR_REG_RUNNING 0
+#define DRR_REG_CONVERGED 1
+#define DRR_REG_FAILED 2
+#define DRR_REG_DONE 3
+
+/* One registration iteration `iter` for B independent registrations: records
+ * (pose[1:], loss) into the traces (B x (max_iters+1) x 6 and
+ * B x (max_iters+1)), sets the state on convergence / failure / last
+ * iteration, else applies v <- m v - beta * grad[1:], eta[1:] += v. */
+int drr_register_update(double *d_eta, double *d_velocity,
+                        const double *d_grad_frames, const double *d_value,
+                        const int *d_loss_status, const drr_reg_config *cfg,
+                        int32_t iter, int *d_state, int *d_n_records,
+                        double *d_trace_eta, double *d_trace_loss,
+                        int32_t n_poses, void *stream);
 
 #ifdef __cplusplus
 }

@@ -35,6 +35,10 @@ EXPORTS = (
     "drr_backward_workspace_size",
     "drr_backward",
     "drr_count_steps",
+    "drr_pose_frames",
+    "drr_pose_grad",
+    "drr_image_loss",
+    "drr_register_update",
 )
 
 
@@ -42,6 +46,14 @@ class DrrGrid(ctypes.Structure):
     _fields_ = [("dims", ctypes.c_int64 * 3),
                 ("spacing", ctypes.c_double * 3),
                 ("origin", ctypes.c_double * 3)]
+
+
+class DrrRegConfig(ctypes.Structure):
+    _fields_ = [("lr_rotation", ctypes.c_double),
+                ("lr_translation", ctypes.c_double),
+                ("momentum", ctypes.c_double),
+                ("converged_threshold", ctypes.c_double),
+                ("max_iters", ctypes.c_int32)]
 
 
 class DrrDetector(ctypes.Structure):
@@ -68,7 +80,16 @@ _SIGNATURES = {
     "drr_backward_workspace_size": ([_i32, _DP], _sz),
     "drr_backward": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp, _vp, _int, _vp, _sz, _vp], _int),
     "drr_count_steps": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
+    "drr_pose_frames": ([_vp, _i32, ctypes.POINTER(ctypes.c_double), _vp, _vp], _int),
+    "drr_pose_grad": ([_vp, _vp, _i32, _vp, _vp], _int),
+    "drr_image_loss": ([_vp, _vp, _int, _i64, _i32, _i64, _int, _vp, _vp, _vp, _vp], _int),
+    "drr_register_update": ([_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(DrrRegConfig), _i32,
+                             _vp, _vp, _vp, _vp, _i32, _vp], _int),
 }
+
+DRR_LOSS_NEG_ZNCC = 0
+DRR_LOSS_L2 = 1
+DRR_REG_RUNNING, DRR_REG_CONVERGED, DRR_REG_FAILED, DRR_REG_DONE = 0, 1, 2, 3
 
 _lib = None
 

@@ -23,6 +23,8 @@
 
 #include "../../include/drr_b200.h"
 #include "siddon_walk.cuh"
+#include "loss_kernels.cuh"
+#include "pose_kernels.cuh"
 
 namespace drr {
 
@@ -612,6 +614,76 @@ int drr_count_steps(const void* d_vol, int vol_dtype, const drr_grid* grid,
   else
     return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
   return check_launch("drr_count_steps");
+}
+
+int drr_pose_frames(const double* d_eta, int32_t n_poses, const double* isocenter,
+                    double* d_frames, void* stream) {
+  if (n_poses < 0) return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses < 0");
+  if (isocenter == nullptr) return fail(DRR_ERR_INVALID_ARGUMENT, "isocenter is NULL");
+  if (n_poses == 0) return DRR_OK;
+  const int th = 128;
+  drr::k_pose_frames<<<(n_poses + th - 1) / th, th, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_eta, isocenter[0], isocenter[1], isocenter[2], n_poses, d_frames);
+  return check_launch("drr_pose_frames");
+}
+
+int drr_pose_grad(const double* d_eta, const double* d_grad_frames, int32_t n_poses,
+                  double* d_grad_eta, void* stream) {
+  if (n_poses < 0) return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses < 0");
+  if (n_poses == 0) return DRR_OK;
+  const int th = 128;
+  drr::k_pose_grad<<<(n_poses + th - 1) / th, th, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_eta, d_grad_frames, n_poses, d_grad_eta);
+  return check_launch("drr_pose_grad");
+}
+
+int drr_image_loss(const void* d_img, const void* d_fixed, int img_dtype, int64_t fixed_stride,
+                   int32_t n_images, int64_t npix, int kind, double* d_value, float* d_grad,
+                   int* d_status, void* stream) {
+  if (n_images < 0 || npix < 1)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "need n_images >= 0 and npix >= 1");
+  if (kind != DRR_LOSS_NEG_ZNCC && kind != DRR_LOSS_L2)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "loss kind must be neg_zncc (0) or l2 (1), got %d", kind);
+  if (fixed_stride != 0 && fixed_stride != npix)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "fixed_stride must be 0 or npix");
+  if (n_images == 0) return DRR_OK;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (img_dtype == 0)
+    drr::k_image_loss<float><<<n_images, drr::kLossThreads, 0, st>>>(
+        static_cast<const float*>(d_img), static_cast<const float*>(d_fixed), fixed_stride, npix,
+        kind, d_value, d_grad, d_status);
+  else if (img_dtype == 1)
+    drr::k_image_loss<double><<<n_images, drr::kLossThreads, 0, st>>>(
+        static_cast<const double*>(d_img), static_cast<const double*>(d_fixed), fixed_stride,
+        npix, kind, d_value, d_grad, d_status);
+  else
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown img_dtype %d", img_dtype);
+  return check_launch("drr_image_loss");
+}
+
+int drr_register_update(double* d_eta, double* d_velocity, const double* d_grad_frames,
+                        const double* d_value, const int* d_loss_status,
+                        const drr_reg_config* cfg, int32_t iter, int* d_state, int* d_n_records,
+                        double* d_trace_eta, double* d_trace_loss, int32_t n_poses,
+                        void* stream) {
+  if (cfg == nullptr) return fail(DRR_ERR_INVALID_ARGUMENT, "cfg is NULL");
+  if (!(cfg->lr_rotation > 0) || !(cfg->lr_translation > 0))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "learning rates must be positive");
+  if (!(cfg->momentum >= 0.0 && cfg->momentum < 1.0))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "momentum must be in [0, 1), got %g", cfg->momentum);
+  if (cfg->max_iters < 1)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "max_iters must be >= 1, got %d", cfg->max_iters);
+  if (iter < 0 || iter > cfg->max_iters)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "iter %d outside [0, max_iters]", iter);
+  if (n_poses < 0) return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses < 0");
+  if (n_poses == 0) return DRR_OK;
+  drr::RegConfig c{cfg->lr_rotation, cfg->lr_translation, cfg->momentum,
+                   cfg->converged_threshold, cfg->max_iters};
+  const int th = 128;
+  drr::k_register_update<<<(n_poses + th - 1) / th, th, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_eta, d_velocity, d_grad_frames, d_value, d_loss_status, c, iter, d_state, d_n_records,
+      d_trace_eta, d_trace_loss, n_poses);
+  return check_launch("drr_register_update");
 }
 
 }  // extern "C"

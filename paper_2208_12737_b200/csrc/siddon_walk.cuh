@@ -522,10 +522,15 @@ struct GradVisitor {
   double pend = 0.0;  // value of the used segment ending at the next crossing
   double G0 = 0.0, G1 = 0.0, G2 = 0.0, H0 = 0.0, H1 = 0.0, H2 = 0.0;
   __device__ __forceinline__ void apply(int label, double alpha, double c) {
-    // predicated per-axis accumulation (label 3 = clip: no tangent)
-    if (label == 0) { G0 += c; H0 = __fma_rn(c, alpha, H0); }
-    if (label == 1) { G1 += c; H1 = __fma_rn(c, alpha, H1); }
-    if (label == 2) { G2 += c; H2 = __fma_rn(c, alpha, H2); }
+    // per-axis accumulation via selects (label 3 = clip: no tangent); measured
+    // faster than predicated branches (profiles/r01_v2 A/B)
+    const double c0 = label == 0 ? c : 0.0;
+    const double c1 = label == 1 ? c : 0.0;
+    const double c2 = label == 2 ? c : 0.0;
+    G0 += c0; G1 += c1; G2 += c2;
+    H0 = __fma_rn(c0, alpha, H0);
+    H1 = __fma_rn(c1, alpha, H1);
+    H2 = __fma_rn(c2, alpha, H2);
   }
   __device__ __forceinline__ void segment(bool used, double seg, double v,
                                           int lab_start, double a_start) {

@@ -1,0 +1,256 @@
+"""Loss + gradient and slice-to-volume registration on the device.
+
+Mirrors the reference's ``gradients.loss_and_gradient`` (``gradients.py:61-69``)
+and ``registration.register`` (``registration.py:89-125``), batched:
+
+* :func:`loss_and_gradient` -- B poses at once: ``drr_pose_frames`` ->
+  ``drr_forward`` -> ``drr_image_loss`` (fused neg-ZNCC / L2 value + pixel
+  gradient) -> ``drr_backward`` -> ``drr_pose_grad``.  Five native launches,
+  no host round trip, no torch autograd.
+* :class:`RegistrationEngine` -- B independent momentum-GD registrations
+  (``OptimizerConfig`` defaults = the paper's hyper-parameters,
+  ``registration.py:41-58``).  Each iteration is the five launches above plus
+  ``drr_register_update``, which keeps the reference's convergence / failure
+  bookkeeping on the device; the whole ``max_iters + 1`` loop is captured in
+  one CUDA graph.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import InvalidArgumentError
+from .renderer import Detector, DeviceVolume
+
+LOSS_KINDS = {"neg_zncc": _lib.DRR_LOSS_NEG_ZNCC, "l2": _lib.DRR_LOSS_L2}
+
+
+@dataclass
+class OptimizerConfig:
+    """registration.py:41-58 (paper section 3.2 hyper-parameters)."""
+
+    lr_rotation: float = 5.3e-2
+    lr_translation: float = 7.5e1
+    momentum: float = 0.9
+    max_iters: int = 250
+    converged_threshold: float = -0.999
+    loss_kind: str = "neg_zncc"
+
+    def __post_init__(self):
+        if self.lr_rotation <= 0 or self.lr_translation <= 0:
+            raise InvalidArgumentError("learning rates must be positive")
+        if not 0.0 <= self.momentum < 1.0:
+            raise InvalidArgumentError(f"momentum must be in [0, 1), got {self.momentum}")
+        if self.max_iters < 1:
+            raise InvalidArgumentError(f"max_iters must be >= 1, got {self.max_iters}")
+        if self.loss_kind not in LOSS_KINDS:
+            raise InvalidArgumentError(f"loss kind must be one of {tuple(LOSS_KINDS)}")
+
+    def c(self):
+        cfg = _lib.DrrRegConfig()
+        cfg.lr_rotation = self.lr_rotation
+        cfg.lr_translation = self.lr_translation
+        cfg.momentum = self.momentum
+        cfg.converged_threshold = self.converged_threshold
+        cfg.max_iters = self.max_iters
+        return cfg
+
+
+@dataclass
+class RegistrationTrace:
+    """registration.py:61-86: per-iteration (theta..bz) and losses."""
+
+    rho: float
+    poses: np.ndarray
+    losses: np.ndarray
+    converged: bool
+    failed: bool = False
+
+    @property
+    def iterations_used(self) -> int:
+        return len(self.losses) - 1
+
+    @property
+    def final_loss(self) -> float:
+        return float(self.losses[-1])
+
+
+def _stream(dev) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+class _Buffers:
+    """Device buffers for B poses; reused across calls (no allocation in the loop)."""
+
+    def __init__(self, vol: DeviceVolume, det: Detector, B: int):
+        dev = vol.device
+        self.B = B
+        self.frames = torch.empty((B, 12), dtype=torch.float64, device=dev)
+        self.img = torch.empty((B, det.height, det.width), dtype=torch.float32, device=dev)
+        self.pix_grad = torch.empty_like(self.img)
+        self.value = torch.empty(B, dtype=torch.float64, device=dev)
+        self.status = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.grad_frames = torch.empty((B, 12), dtype=torch.float64, device=dev)
+        self.grad_eta = torch.empty((B, 7), dtype=torch.float64, device=dev)
+        lib = _lib.load()
+        self.ws_bytes = lib.drr_backward_workspace_size(B, det.c)
+        self.ws = torch.empty(max(self.ws_bytes, 8), dtype=torch.uint8, device=dev)
+
+
+def _launch_loss_grad(lib, vol, det, iso, eta, fixed, fixed_stride, kind, buf, stream):
+    B = buf.B
+    _lib.check(lib.drr_pose_frames(eta.data_ptr(), B, iso, buf.frames.data_ptr(), stream))
+    _lib.check(lib.drr_forward(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
+                               buf.frames.data_ptr(), B, det.c, buf.img.data_ptr(), 0, stream))
+    _lib.check(lib.drr_image_loss(buf.img.data_ptr(), fixed.data_ptr(), 0, fixed_stride, B,
+                                  det.height * det.width, kind, buf.value.data_ptr(),
+                                  buf.pix_grad.data_ptr(), buf.status.data_ptr(), stream))
+    _lib.check(lib.drr_backward(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
+                                buf.frames.data_ptr(), B, det.c, buf.pix_grad.data_ptr(), 0,
+                                buf.grad_frames.data_ptr(), None, 0, buf.ws.data_ptr(),
+                                buf.ws_bytes, stream))
+
+
+def _prep_fixed(fixed, B, det, dev):
+    fixed = torch.as_tensor(fixed, device=dev, dtype=torch.float32)
+    if fixed.shape[-2:] != (det.height, det.width):
+        raise InvalidArgumentError(
+            f"fixed image shape {tuple(fixed.shape)} does not match detector {det.height}x{det.width}")
+    if fixed.ndim == 2 or fixed.shape[0] == 1:
+        return fixed.reshape(det.height, det.width).contiguous(), 0
+    if fixed.shape[0] != B:
+        raise InvalidArgumentError(f"need 1 or {B} fixed images, got {fixed.shape[0]}")
+    return fixed.contiguous(), det.height * det.width
+
+
+def loss_and_gradient(vol: DeviceVolume, det: Detector, eta, fixed, loss_kind: str = "neg_zncc",
+                      isocenter=None, buffers: _Buffers | None = None):
+    """Batched ``gradients.loss_and_gradient``: (value (B,), grad (B, 7)) for
+    pose vectors eta (B, 7) = (rho, theta, phi, gamma, bx, by, bz).
+
+    Device tensors in and out; undefined metrics give NaN values (status in
+    ``buffers.status``) instead of raising, so the call never synchronises."""
+    if loss_kind not in LOSS_KINDS:
+        raise InvalidArgumentError(f"loss kind must be one of {tuple(LOSS_KINDS)}, got {loss_kind!r}")
+    dev = vol.device
+    eta = torch.as_tensor(eta, device=dev, dtype=torch.float64)
+    if eta.ndim == 1:
+        eta = eta[None]
+    eta = eta.contiguous()
+    B = eta.shape[0]
+    buf = buffers if buffers is not None and buffers.B == B else _Buffers(vol, det, B)
+    fixed_t, stride = _prep_fixed(fixed, B, det, dev)
+    iso = _iso(vol, isocenter)
+    lib = _lib.load()
+    st = _stream(dev)
+    _launch_loss_grad(lib, vol, det, iso, eta, fixed_t, stride, LOSS_KINDS[loss_kind], buf, st)
+    _lib.check(lib.drr_pose_grad(eta.data_ptr(), buf.grad_frames.data_ptr(), B,
+                                 buf.grad_eta.data_ptr(), st))
+    return buf.value.clone(), buf.grad_eta.clone()
+
+
+def _iso(vol, isocenter):
+    import ctypes
+    c = vol.center if isocenter is None else tuple(float(v) for v in isocenter)
+    return (ctypes.c_double * 3)(*c)
+
+
+class RegistrationEngine:
+    """B independent registrations of fixed image(s) against one CT volume."""
+
+    def __init__(self, vol: DeviceVolume, det: Detector, fixed, B: int = 1,
+                 config: OptimizerConfig | None = None, isocenter=None):
+        self.vol, self.det, self.B = vol, det, int(B)
+        self.config = config or OptimizerConfig()
+        dev = vol.device
+        self.fixed, self.fixed_stride = _prep_fixed(fixed, self.B, det, dev)
+        self.iso = _iso(vol, isocenter)
+        self.buf = _Buffers(vol, det, self.B)
+        T = self.config.max_iters + 1
+        self.eta = torch.zeros((self.B, 7), dtype=torch.float64, device=dev)
+        self.vel = torch.zeros((self.B, 6), dtype=torch.float64, device=dev)
+        self.state = torch.zeros(self.B, dtype=torch.int32, device=dev)
+        self.n_rec = torch.zeros(self.B, dtype=torch.int32, device=dev)
+        self.trace_eta = torch.zeros((self.B, T, 6), dtype=torch.float64, device=dev)
+        self.trace_loss = torch.zeros((self.B, T), dtype=torch.float64, device=dev)
+        self.graph = None
+        self.kind = LOSS_KINDS[self.config.loss_kind]
+        self._cfg = self.config.c()
+
+    def reset(self, poses0):
+        p = torch.as_tensor(poses0, dtype=torch.float64, device=self.vol.device).reshape(self.B, 7)
+        self.eta.copy_(p)
+        self.vel.zero_()
+        self.state.zero_()
+        self.n_rec.zero_()
+
+    def _iteration(self, it: int, stream: int):
+        lib = _lib.load()
+        _launch_loss_grad(lib, self.vol, self.det, self.iso, self.eta, self.fixed,
+                          self.fixed_stride, self.kind, self.buf, stream)
+        _lib.check(lib.drr_register_update(
+            self.eta.data_ptr(), self.vel.data_ptr(), self.buf.grad_frames.data_ptr(),
+            self.buf.value.data_ptr(), self.buf.status.data_ptr(), self._cfg, it,
+            self.state.data_ptr(), self.n_rec.data_ptr(), self.trace_eta.data_ptr(),
+            self.trace_loss.data_ptr(), self.B, stream))
+
+    def run(self, use_graph: bool = True):
+        """All max_iters + 1 iterations (converged / failed registrations are
+        frozen on the device).  With use_graph the loop is one CUDA graph."""
+        dev = self.vol.device
+        if not use_graph:
+            st = _stream(dev)
+            for it in range(self.config.max_iters + 1):
+                self._iteration(it, st)
+            return
+        if self.graph is None:
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):  # warm-up outside capture (loads the module)
+                self._iteration(0, side.cuda_stream)
+            torch.cuda.current_stream(dev).wait_stream(side)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                st = _stream(dev)
+                for it in range(self.config.max_iters + 1):
+                    self._iteration(it, st)
+        self.graph.replay()
+
+    def traces(self):
+        n = self.n_rec.cpu().numpy()
+        state = self.state.cpu().numpy()
+        te = self.trace_eta.cpu().numpy()
+        tl = self.trace_loss.cpu().numpy()
+        rho = self.eta[:, 0].cpu().numpy()
+        out = []
+        for b in range(self.B):
+            k = int(n[b])
+            out.append(RegistrationTrace(rho=float(rho[b]), poses=te[b, :k].copy(),
+                                         losses=tl[b, :k].copy(),
+                                         converged=bool(state[b] == _lib.DRR_REG_CONVERGED),
+                                         failed=bool(state[b] == _lib.DRR_REG_FAILED)))
+        return out
+
+
+def register(fixed_image, vol: DeviceVolume, pose0, det: Detector,
+             config: OptimizerConfig | None = None, use_graph: bool = False) -> RegistrationTrace:
+    """``registration.register`` for one pose vector (rho, theta, ..., bz)."""
+    eng = RegistrationEngine(vol, det, fixed_image, 1, config)
+    eng.reset(np.asarray(pose0, dtype=np.float64)[None])
+    eng.run(use_graph=use_graph)
+    return eng.traces()[0]
+
+
+def register_batch(fixed_images, vol: DeviceVolume, poses0, det: Detector,
+                   config: OptimizerConfig | None = None, use_graph: bool = True):
+    """B independent registrations (the population study, cli.py:133-145)."""
+    poses0 = np.asarray(poses0, dtype=np.float64).reshape(-1, 7)
+    eng = RegistrationEngine(vol, det, fixed_images, poses0.shape[0], config)
+    eng.reset(poses0)
+    eng.run(use_graph=use_graph)
+    return eng.traces()
