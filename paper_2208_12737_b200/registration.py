@@ -209,11 +209,14 @@ class RegistrationEngine:
                 self._iteration(it, st)
             return
         if self.graph is None:
+            saved = [t.clone() for t in (self.eta, self.vel, self.state, self.n_rec)]
             side = torch.cuda.Stream(dev)
             side.wait_stream(torch.cuda.current_stream(dev))
-            with torch.cuda.stream(side):  # warm-up outside capture (loads the module)
+            with torch.cuda.stream(side):  # warm-up outside capture (loads the kernels)
                 self._iteration(0, side.cuda_stream)
             torch.cuda.current_stream(dev).wait_stream(side)
+            for t, s in zip((self.eta, self.vel, self.state, self.n_rec), saved):
+                t.copy_(s)  # the warm-up iteration must not advance the registrations
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph):
                 st = _stream(dev)
