@@ -228,35 +228,52 @@ def main():
         fixed = drr(torch.tensor(TRUTH[1:4], device=dev), torch.tensor(TRUTH[4:7], device=dev))
     fixed_b = fixed.expand(B, H, W)
 
-    def step(rot, tra):
+    from paper_2208_12737_b200.registration import _Buffers, loss_and_gradient
+
+    eta0 = torch.tensor(poses_np, device=dev)
+    bufs = _Buffers(drr.volume, drr.detector, B)
+
+    def step(eta):
+        # the reference's unit of work, batched: loss_and_gradient
+        # (gradients.py:61-69) = pose frames -> forward -> fused neg-ZNCC + pixel
+        # gradient -> fused backward re-walk -> pose gradient (6 native launches)
+        return loss_and_gradient(drr.volume, drr.detector, eta, fixed, "neg_zncc", buffers=bufs)
+
+    def module_step(rot, tra):
+        # the north-star nn.Module path (torch autograd around drr_forward/backward)
         rot = rot.detach().requires_grad_(True)
         tra = tra.detach().requires_grad_(True)
-        img = drr(rot, tra)
-        loss = neg_zncc(img, fixed_b)
+        loss = neg_zncc(drr(rot, tra), fixed_b)
         loss.sum().backward()
         return loss.detach(), rot.grad, tra.grad
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    # --- warmup + timed steps (device time, per-step events) -------------
-    for _ in range(max(args.warmup, 3)):
-        step(rot0, tra0)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    times = []
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
+    def timed(fn, n, warm):
+        out = []
+        for i in range(n + warm):
             flush.fill_(1.0)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step(rot0, tra0)
+            fn()
             e1.record(stream)
             e1.synchronize()
-            times.append(e0.elapsed_time(e1))
+            if i >= warm:
+                out.append(e0.elapsed_time(e1))
+        return out
+
+    # --- warmup + timed steps (device time, per-step events) -------------
+    for _ in range(max(args.warmup, 3)):
+        step(eta0)
+        module_step(rot0, tra0)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        times = timed(lambda: step(eta0), args.steps, 0)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -266,29 +283,24 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item())
     value = B * world / (ms_per_step / 1e3)
+    module_ms = float(np.mean(timed(lambda: module_step(rot0, tra0), max(10, args.steps // 5), 2)))
 
     # --- e2e: public API with pinned host poses in, loss+grads out -------
-    h_rot = torch.tensor(poses_np[:, 1:4]).pin_memory()
-    h_tra = torch.tensor(poses_np[:, 4:7]).pin_memory()
-    h_out = torch.empty((B, 7), dtype=torch.float64).pin_memory()
-    e2e_times = []
-    for i in range(args.steps + 3):
-        flush.fill_(1.0)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rot = h_rot.to(dev, non_blocking=True)
-        tra = h_tra.to(dev, non_blocking=True)
-        loss, gr, gt = step(rot, tra)
-        h_out.copy_(torch.cat([loss[:, None], gr, gt], dim=1), non_blocking=True)
-        e1.record(stream)
-        e1.synchronize()
-        if i >= 3:
-            e2e_times.append(e0.elapsed_time(e1))
-    e = torch.tensor([float(np.mean(e2e_times))], device=dev, dtype=torch.float64)
+    h_eta = torch.tensor(poses_np).pin_memory()
+    h_out = torch.empty((B, 8), dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        eta = h_eta.to(dev, non_blocking=True)
+        val, grad = step(eta)
+        h_out.copy_(torch.cat([val[:, None], grad], dim=1), non_blocking=True)
+
+    e = torch.tensor([float(np.mean(timed(e2e_step, args.steps, 3)))], device=dev,
+                     dtype=torch.float64)
     if world > 1:
         dist.all_reduce(e, op=dist.ReduceOp.MAX)
     e2e_value = B * world / (float(e.item()) / 1e3)
+    rot0 = eta0[:, 1:4]
+    tra0 = eta0[:, 4:7]
 
     # --- roofline of the dominant kernel (k_backward) --------------------
     frames = pose_frames(drr.pose_vectors(rot0, tra0), drr.isocenter).detach()
@@ -328,19 +340,22 @@ def main():
     achieved_bwd = bytes_bwd / (bwd_ms / 1e3) / 1e9
 
     # single-pose latency (C2 as configs[1] states it: one pose fwd+bwd)
-    one = []
-    for i in range(10):
-        flush.fill_(1.0)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rr = rot0[:1].detach().requires_grad_(True)
-        tt = tra0[:1].detach().requires_grad_(True)
-        neg_zncc(drr(rr, tt), fixed[None]).sum().backward()
-        e1.record(stream)
-        e1.synchronize()
-        if i >= 3:
-            one.append(e0.elapsed_time(e1))
+    bufs1 = _Buffers(drr.volume, drr.detector, 1)
+    one = timed(lambda: loss_and_gradient(drr.volume, drr.detector, eta0[:1], fixed, "neg_zncc",
+                                          buffers=bufs1), 10, 3)
+    # C3: 250-step registration, whole loop in one CUDA graph
+    from paper_2208_12737_b200.registration import OptimizerConfig, RegistrationEngine
+    reg_cfg = OptimizerConfig(converged_threshold=-1.1)
+    eng = RegistrationEngine(drr.volume, drr.detector, fixed, 1, reg_cfg)
+    eng.reset(poses_np[:1])
+    eng.run(use_graph=True)
+
+    def reg_run():
+        eng.reset(poses_np[:1])
+        eng.run(use_graph=True)
+
+    reg_ms = float(np.median(timed(reg_run, 3, 1)))
+    reg_final = eng.traces()[0].final_loss
 
     if world > 1:
         dist.barrier()
@@ -366,9 +381,11 @@ def main():
                    "detector": [H, W], "ct": list(DIMS), "parallelism": f"pose-shard x{world}",
                    "l2": "flushed (256 MiB write) between timed steps, outside the events"},
         "e2e": {"value": e2e_value, "unit": "DRR/s",
-                "h2d_bytes_per_step": int(h_rot.numel() * 8 + h_tra.numel() * 8),
+                "h2d_bytes_per_step": int(h_eta.numel() * 8),
                 "d2h_bytes_per_step": int(h_out.numel() * 8)},
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": 6 * args.steps,
+        "module_path": {"api": "DRR nn.Module + torch neg_zncc + autograd",
+                        "ms_per_step": module_ms, "value": B / (module_ms / 1e3)},
         "roofline": {"bound": "hbm", "kernel": "k_backward (fused re-walk + frame reduction)",
                      "achieved": achieved_bwd, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved_bwd / hbm_peak, "traffic": None,
@@ -379,6 +396,9 @@ def main():
                     "voxel_steps_per_s_fwd": S / (fwd_ms / 1e3),
                     "fwd_achieved_gbs": bytes_fwd / (fwd_ms / 1e3) / 1e9},
         "single_pose_fwd_bwd_ms": float(np.mean(one)),
+        "registration_c3": {"steps": reg_cfg.max_iters + 1, "ms_total": reg_ms,
+                            "ms_per_step": reg_ms / (reg_cfg.max_iters + 1),
+                            "final_neg_zncc": reg_final, "cuda_graph": True},
         "clocks": clocks,
     }
     if not args.no_cpu_baseline and world == 1:
