@@ -142,11 +142,30 @@ __global__ void DRR_LB
 
 // Endpoint gradients of one ray from the reverse-mode visitor
 // (see orc_raysum_endpoint_grad in oracle/siddon_oracle.c for the algebra).
+__device__ __forceinline__ void visitor_sums(const GradVisitor& v, double* G, double* Hh) {
+  G[0] = v.G0; G[1] = v.G1; G[2] = v.G2;
+  Hh[0] = v.H0; Hh[1] = v.H1; Hh[2] = v.H2;
+}
+__device__ __forceinline__ void visitor_sums(const GradVisitorSmem& v, double* G, double* Hh) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) { G[a] = v.G(a); Hh[a] = v.H(a); }
+}
+
+#if DRR_GRAD_SMEM
+using BwdVisitor = GradVisitorSmem;
+#else
+using BwdVisitor = GradVisitor;
+#endif
+
+__device__ __forceinline__ void visitor_init(GradVisitor&, double*) {}
+__device__ __forceinline__ void visitor_init(GradVisitorSmem& v, double* slots) { v.init(slots); }
+
+template <typename V>
 __device__ __forceinline__ void endpoint_grads(const Ray& r,
-                                               const GradVisitor& v, double L,
+                                               const V& v, double L,
                                                double* dEds, double* dEdp) {
-  const double G[3] = {v.G0, v.G1, v.G2};
-  const double Hh[3] = {v.H0, v.H1, v.H2};
+  double G[3], Hh[3];
+  visitor_sums(v, G, Hh);
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double gs = 0.0, gp = 0.0;
@@ -185,7 +204,8 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
     ray_setup(g, s, p, r);
     double e = 0.0;
     if (r.hit) {
-      GradVisitor vis;
+      BwdVisitor vis;
+      visitor_init(vis, tab + plane_table_len(g) + kWalkSmemDoublesPerThread * 128);
       walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
       const double L = ray_length(r);
       e = L * vis.acc;
@@ -303,7 +323,8 @@ __global__ void __launch_bounds__(kRayThreads)
   ray_setup(g, s, p, r);
   double e = 0.0, gs[3] = {0.0, 0.0, 0.0}, gp[3] = {0.0, 0.0, 0.0};
   if (r.hit) {
-    GradVisitor vis;
+    BwdVisitor vis;
+    visitor_init(vis, tab + plane_table_len(g) + kWalkSmemDoublesPerThread * 128);
     walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
     const double L = ray_length(r);
     e = L * vis.acc;
@@ -343,7 +364,8 @@ int check_launch(const char* what) {
 size_t table_bytes(const drr::GridDev& g) {
   // plane table + the walk's per-thread constants (both kernels use <= 128 threads)
   return (static_cast<size_t>(drr::plane_table_len(g)) +
-          static_cast<size_t>(drr::kWalkSmemDoublesPerThread) * 128) * sizeof(double);
+          static_cast<size_t>(drr::kWalkSmemDoublesPerThread + drr::kGradSmemDoublesPerThread) *
+              128) * sizeof(double);
 }
 
 template <typename Kernel>
