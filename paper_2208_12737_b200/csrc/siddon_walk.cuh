@@ -250,6 +250,21 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
 // selects, so lanes taking different axes never diverge.  The gather of
 // segment i is consumed in iteration i+1 (one-deep software pipeline) so its
 // latency overlaps the next crossing's arithmetic.
+// Gather pipeline depth: segment i's voxel load is consumed in iteration
+// i + kPipe, so up to kPipe gathers per ray are in flight (ncu: the gather's
+// long-scoreboard stall dominated at depth 1).
+#ifndef DRR_PIPE
+#define DRR_PIPE 2
+#endif
+
+template <typename VT>
+struct PipeStage {
+  bool used;
+  double seg, a;
+  int lab;
+  VT v;
+};
+
 template <typename VT, typename Visitor>
 __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
                                             const GridDev& g,
@@ -268,10 +283,11 @@ __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
   int flat = r.flat;
   double prev = r.amin;
   int lab = r.lab_min;
-  bool p_used = false;
-  double p_seg = 0.0, p_a = 0.0;
-  int p_lab = 0;
-  VT p_v = VT(0);
+  // pipe[0] is the oldest in-flight segment; empty stages are unused zero
+  // segments (harmless to every visitor, see GradVisitor::segment).
+  PipeStage<VT> pipe[DRR_PIPE];
+#pragma unroll
+  for (int k = 0; k < DRR_PIPE; ++k) pipe[k] = PipeStage<VT>{false, 0.0, 0.0, 0, VT(0)};
   for (;;) {
     const bool c1 = an1 < an0;
     double best = c1 ? an1 : an0;
@@ -286,12 +302,11 @@ __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
       idx = exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
     VT v = VT(0);
     if (used) v = __ldg(vol + idx);
-    vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
-    p_used = used;
-    p_seg = seg;
-    p_v = v;
-    p_lab = lab;
-    p_a = prev;
+    vis.segment(pipe[0].used, pipe[0].seg, static_cast<double>(pipe[0].v), pipe[0].lab,
+                pipe[0].a);
+#pragma unroll
+    for (int k = 0; k + 1 < DRR_PIPE; ++k) pipe[k] = pipe[k + 1];
+    pipe[DRR_PIPE - 1] = PipeStage<VT>{used, seg, prev, lab, v};
     prev = cur;
     if (last) break;
     const double s = c2 ? s2 : (c1 ? s1 : s0);
@@ -310,184 +325,22 @@ __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
     flat += c2 ? df2 : (c1 ? df1 : df0);
     lab = c2 ? 2 : (c1 ? 1 : 0);
   }
-  vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
-  vis.finish(r.lab_max, amax);
-}
-
-// Lookahead variant: every axis carries its next AND next-next crossing
-// parameter; each iteration speculatively computes the crossing after that for
-// all three axes (axis-specific registers, no selects of per-axis constants,
-// full ILP) and commits it only for the crossed axis.  The division is off the
-// loop-carried dependency chain (argmin -> commit).
-template <typename VT, typename Visitor>
-__device__ __forceinline__ void walk_lookahead(const VT* __restrict__ vol,
-                                               const GridDev& g,
-                                               const double* __restrict__ tab,
-                                               const Ray& r, Visitor& vis) {
-  const double s0 = r.s[0], s1 = r.s[1], s2 = r.s[2];
-  const double d0 = r.d[0], d1 = r.d[1], d2 = r.d[2];
-  const double i0 = r.inv[0], i1 = r.inv[1], i2 = r.inv[2];
-  const int st0 = r.st[0], st1 = r.st[1], st2 = r.st[2];
-  const int df0 = st0, df1 = st1 * g.stride[1], df2 = st2 * g.stride[2];
-  const double amax = r.amax, T = r.T;
-  const bool safe = r.safe;
-  const unsigned total = static_cast<unsigned>(g.total);
-  // q_a: table index of the plane AFTER the next one (the next-next plane).
-  int q0 = r.q[0] + st0, q1 = r.q[1] + st1, q2 = r.q[2] + st2;
-  auto alpha = [&](int q, double s, double d, double inv) {
-    const double num = tab[q] - s;
-    return safe ? num / d : div_rn(num, d, inv);
-  };
-  double an0 = r.an[0], an1 = r.an[1], an2 = r.an[2];
-  // parallel axes keep +inf; their q stays parked on P(0) (never read past)
-  double nn0 = st0 ? alpha(q0, s0, d0, i0) : INFINITY;
-  double nn1 = st1 ? alpha(q1, s1, d1, i1) : INFINITY;
-  double nn2 = st2 ? alpha(q2, s2, d2, i2) : INFINITY;
-  // an exhausted axis (next plane is a sentinel) must not read beyond the table
-  if (!(an0 < kSentinel)) { nn0 = kSentinel; q0 -= st0; }
-  if (!(an1 < kSentinel)) { nn1 = kSentinel; q1 -= st1; }
-  if (!(an2 < kSentinel)) { nn2 = kSentinel; q2 -= st2; }
-  int flat = r.flat;
-  double prev = r.amin;
-  int lab = r.lab_min;
-  bool p_used = false;
-  double p_seg = 0.0, p_a = 0.0;
-  int p_lab = 0;
-  VT p_v = VT(0);
-  for (;;) {
-    const bool c1 = an1 < an0;
-    const bool c2 = (an2 < an0) && (an2 < an1);
-    const double best = c2 ? an2 : (c1 ? an1 : an0);
-    const bool last = !(best <= amax);
-    const double cur = last ? amax : best;
-    const double seg = cur - prev;
-    const bool used = seg > kSegEps;
-    int idx = flat;
-    if (used && (!(seg > T) || static_cast<unsigned>(flat) >= total))
-      idx = exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
-    VT v = VT(0);
-    if (used) v = __ldg(vol + idx);
-    vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
-    p_used = used;
-    p_seg = seg;
-    p_v = v;
-    p_lab = lab;
-    p_a = prev;
-    prev = cur;
-    if (last) break;
-    // speculative next-next-next crossings (sentinel slots clamp the index)
-    const int n0 = q0 + st0, n1 = q1 + st1, n2 = q2 + st2;
-    const double x0 = alpha(n0, s0, d0, i0);
-    const double x1 = alpha(n1, s1, d1, i1);
-    const double x2 = alpha(n2, s2, d2, i2);
-    const bool a0 = !(c1 || c2), a1 = c1 && !c2;
-    if (a0) { an0 = nn0; nn0 = x0; q0 = n0; flat += df0; }
-    if (a1) { an1 = nn1; nn1 = x1; q1 = n1; flat += df1; }
-    if (c2) { an2 = nn2; nn2 = x2; q2 = n2; flat += df2; }
-    lab = c2 ? 2 : (c1 ? 1 : 0);
-  }
-  vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
-  vis.finish(r.lab_max, amax);
-}
-
-// Shared-memory-constant variant: each thread parks its per-axis ray
-// constants (s_a, d_a, 1/d_a, walking step) in shared memory, field-major
-// ([field][axis][thread]) so a warp's loads are conflict-free whichever axis
-// each lane crosses; the crossed axis's constants are then 3 LDS.64 + 1 LDS.64
-// instead of 16 ALU selects.  `cst` points at this CTA's block of 4*3*blockDim
-// doubles.
-template <typename VT, typename Visitor>
-__device__ __forceinline__ void walk_smem(const VT* __restrict__ vol,
-                                          const GridDev& g,
-                                          const double* __restrict__ tab,
-                                          double* __restrict__ cst,
-                                          const Ray& r, Visitor& vis) {
-  const int nt = blockDim.x, t = threadIdx.x;
-  double* cs = cst + t;               // s  : cs[a*nt]
-  double* cd = cst + 3 * nt + t;      // d  : cd[a*nt]
-  double* ci = cst + 6 * nt + t;      // inv: ci[a*nt]
-  int2* cx = reinterpret_cast<int2*>(cst + 9 * nt) + t;  // (st, dflat)
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    cs[a * nt] = r.s[a];
-    cd[a * nt] = r.d[a];
-    ci[a * nt] = r.inv[a];
-    cx[a * nt] = make_int2(r.st[a], r.st[a] * g.stride[a]);
-  }
-  double an0 = r.an[0], an1 = r.an[1], an2 = r.an[2];
-  int q0 = r.q[0], q1 = r.q[1], q2 = r.q[2];
-  const double amax = r.amax, T = r.T;
-  const bool safe = r.safe;
-  const unsigned total = static_cast<unsigned>(g.total);
-  int flat = r.flat;
-  double prev = r.amin;
-  int lab = r.lab_min;
-  bool p_used = false;
-  double p_seg = 0.0, p_a = 0.0;
-  int p_lab = 0;
-  VT p_v = VT(0);
-  for (;;) {
-    const bool c1 = an1 < an0;
-    double best = c1 ? an1 : an0;
-    const bool c2 = an2 < best;
-    best = c2 ? an2 : best;
-    const bool last = !(best <= amax);
-    const double cur = last ? amax : best;
-    const double seg = cur - prev;
-    const bool used = seg > kSegEps;
-    int idx = flat;
-    if (used && (!(seg > T) || static_cast<unsigned>(flat) >= total))
-      idx = exact_voxel(g, r.s[0], r.s[1], r.s[2], r.d[0], r.d[1], r.d[2],
-                        0.5 * (prev + cur));
-    VT v = VT(0);
-    if (used) v = __ldg(vol + idx);
-    vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
-    p_used = used;
-    p_seg = seg;
-    p_v = v;
-    p_lab = lab;
-    p_a = prev;
-    prev = cur;
-    if (last) break;
-    const int sel = c2 ? 2 : (c1 ? 1 : 0);
-    const int o = sel * nt;
-    const double s = cs[o], d = cd[o], inv = ci[o];
-    const int2 x = cx[o];
-    const int q = (c2 ? q2 : (c1 ? q1 : q0)) + x.x;
-    const double num = tab[q] - s;
-    const double an = safe ? num / d : div_rn(num, d, inv);
-    const bool a0 = !(c1 || c2), a1 = c1 && !c2;
-    an0 = a0 ? an : an0;
-    an1 = a1 ? an : an1;
-    an2 = c2 ? an : an2;
-    q0 = a0 ? q : q0;
-    q1 = a1 ? q : q1;
-    q2 = c2 ? q : q2;
-    flat += x.y;
-    lab = sel;
-  }
-  vis.segment(p_used, p_seg, static_cast<double>(p_v), p_lab, p_a);
+  for (int k = 0; k < DRR_PIPE; ++k)
+    vis.segment(pipe[k].used, pipe[k].seg, static_cast<double>(pipe[k].v), pipe[k].lab,
+                pipe[k].a);
   vis.finish(r.lab_max, amax);
 }
 
-#ifndef DRR_WALK
-#define DRR_WALK 2
-#endif
-// Per-thread shared-memory doubles the walk needs beyond the plane table.
-constexpr int kWalkSmemDoublesPerThread = (DRR_WALK == 4) ? 12 : 0;
+// Per-thread shared-memory doubles the walk needs beyond the plane table
+// (the smem-constant variant that used them lost the A/B, see profiles/).
+constexpr int kWalkSmemDoublesPerThread = 0;
 
 template <typename VT, typename Visitor>
 __device__ __forceinline__ void walk(const VT* __restrict__ vol, const GridDev& g,
-                                     const double* __restrict__ tab,
-                                     double* __restrict__ cst, const Ray& r,
-                                     Visitor& vis) {
-#if DRR_WALK == 3
-  walk_lookahead<VT>(vol, g, tab, r, vis);
-#elif DRR_WALK == 4
-  walk_smem<VT>(vol, g, tab, cst, r, vis);
-#else
+                                     const double* __restrict__ tab, double* /*cst*/,
+                                     const Ray& r, Visitor& vis) {
   walk_select<VT>(vol, g, tab, r, vis);
-#endif
 }
 
 // ---- visitors ----------------------------------------------------------
