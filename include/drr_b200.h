@@ -62,12 +62,18 @@ typedef struct drr_grid {
 } drr_grid;
 
 /* Detector: H x W pixels, pitch_x along W, pitch_y along H (geometry.py:71-97,
- * 152-157).  Pixel (h, w) sits at c + a_h e1 + a_w e2. */
+ * 152-157).  Pixel (h, w) sits at c + a_h e1 + a_w e2.
+ * ray_split: threads per ray for the batched kernels -- 1 = one thread walks
+ * the whole ray (bit-identical to the reference's sequential sum), 2/4/8 =
+ * the ray is cut at dominant-axis crossings and the chunk sums combined
+ * (same segments, different summation order: ~1e-16 relative), 0 = auto
+ * (split only when B*H*W rays cannot fill the GPU, e.g. one pose). */
 typedef struct drr_detector {
   int32_t height;
   int32_t width;
   double pitch_x;
   double pitch_y;
+  int32_t ray_split;
 } drr_detector;
 
 /* Frames: B x 12 float64, per pose (s[3], c[3], e1[3], e2[3]) in volume

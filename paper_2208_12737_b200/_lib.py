@@ -60,7 +60,8 @@ class DrrDetector(ctypes.Structure):
     _fields_ = [("height", ctypes.c_int32),
                 ("width", ctypes.c_int32),
                 ("pitch_x", ctypes.c_double),
-                ("pitch_y", ctypes.c_double)]
+                ("pitch_y", ctypes.c_double),
+                ("ray_split", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p
@@ -134,10 +135,11 @@ def make_grid(dims, spacing, origin) -> DrrGrid:
     return g
 
 
-def make_detector(height, width, pitch_x, pitch_y) -> DrrDetector:
+def make_detector(height, width, pitch_x, pitch_y, ray_split: int = 0) -> DrrDetector:
     d = DrrDetector()
     d.height = int(height)
     d.width = int(width)
     d.pitch_x = float(pitch_x)
     d.pitch_y = float(pitch_y)
+    d.ray_split = int(ray_split)
     return d

@@ -44,22 +44,47 @@ namespace drr {
 #ifndef DRR_BWD_MINB
 #define DRR_BWD_MINB 5
 #endif
-constexpr int kTileW = 16;
-constexpr int kTileH = 8;
-constexpr int kThreads = kTileW * kTileH;  // 4 warps, each an 8 x 4 quad
+constexpr int kThreads = 128;  // 4 warps per CTA
 constexpr int kFrameGrads = 12;
 
-// Lane -> pixel inside a 16 x 8 CTA tile: warp w covers the 8 x 4 quad
-// (w & 1, w >> 1); lanes are row-major inside the quad.
-__device__ __forceinline__ void tile_pixel(int& h, int& w) {
+// CTA pixel tile for K threads per ray (SURVEY 7 H2 ray splitting):
+//   K = 1: 16 x 8 pixels, each warp an 8 x 4 quad (neighbouring rays share
+//          L1/L2 lines of the CT);
+//   K > 1: 128 / K rays as an 8 x (16 / K) tile; the K chunks of a ray are K
+//          consecutive lanes of one warp, combined with xor shuffles.
+template <int K>
+struct Tile {
+  static constexpr int W = K == 1 ? 16 : 8;
+  static constexpr int H = K == 1 ? 8 : 16 / K;
+};
+
+template <int K>
+__device__ __forceinline__ void tile_ray(int& h, int& w, int& chunk) {
   const int t = threadIdx.x;
-  const int warp = t >> 5, lane = t & 31;
-  w = blockIdx.x * kTileW + (warp & 1) * 8 + (lane & 7);
-  h = blockIdx.y * kTileH + (warp >> 1) * 4 + (lane >> 3);
+  if (K == 1) {
+    const int warp = t >> 5, lane = t & 31;
+    w = blockIdx.x * Tile<K>::W + (warp & 1) * 8 + (lane & 7);
+    h = blockIdx.y * Tile<K>::H + (warp >> 1) * 4 + (lane >> 3);
+    chunk = 0;
+  } else {
+    const int ray = t / K;
+    chunk = t % K;
+    w = blockIdx.x * Tile<K>::W + (ray & 7);
+    h = blockIdx.y * Tile<K>::H + (ray >> 3);
+  }
+}
+
+// Fixed-order sum over the K lanes of a ray (all 32 lanes must call it).
+template <int K, typename T>
+__device__ __forceinline__ T chunk_sum(T x) {
+#pragma unroll
+  for (int off = K / 2; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+  return x;
 }
 
 struct DetDev {
   int H, W;
+  int split;  // requested threads per ray (0 = auto)
   double pitch_x, pitch_y;
   double half_h, half_w;  // (H-1)/2.0, (W-1)/2.0   (geometry.py:155-156)
 };
@@ -90,7 +115,7 @@ __device__ __forceinline__ void store_out(OT* p, double v) {
 }
 
 // ---------------------------------------------------------------- forward
-template <typename VT, typename OT>
+template <typename VT, typename OT, int K>
 __global__ void DRR_LB
     k_forward(const VT* __restrict__ vol, const GridDev g,
               const double* __restrict__ frames, const DetDev det,
@@ -98,24 +123,30 @@ __global__ void DRR_LB
   extern __shared__ double tab[];
   build_plane_table(g, tab);
   __syncthreads();
-  int h, w;
-  tile_pixel(h, w);
-  if (h >= det.H || w >= det.W) return;
+  int h, w, chunk;
+  tile_ray<K>(h, w, chunk);
+  const bool valid = h < det.H && w < det.W;
+  if (K == 1 && !valid) return;
   const int b = blockIdx.z;
-  double s[3], p[3], ah, aw;
-  pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
-  Ray r;
-  ray_setup(g, s, p, r);
-  double e = 0.0;
-  if (r.hit) {
-    SumVisitor vis;
-    walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
-    e = ray_length(r) * vis.acc;
+  double acc = 0.0, L = 0.0;
+  if (valid) {
+    double s[3], p[3], ah, aw;
+    pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
+    Ray r;
+    ray_setup(g, s, p, r, K, chunk);
+    L = ray_length(r);
+    if (r.hit) {
+      SumVisitor vis;
+      walk<VT, (K > 1)>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
+      acc = vis.acc;
+    }
   }
-  store_out(img + (static_cast<size_t>(b) * det.H + h) * det.W + w, e);
+  acc = chunk_sum<K>(acc);
+  if (valid && chunk == 0)
+    store_out(img + (static_cast<size_t>(b) * det.H + h) * det.W + w, L * acc);
 }
 
-template <typename VT>
+template <typename VT, int K>
 __global__ void DRR_LB
     k_count(const VT* __restrict__ vol, const GridDev g,
             const double* __restrict__ frames, const DetDev det,
@@ -123,21 +154,25 @@ __global__ void DRR_LB
   extern __shared__ double tab[];
   build_plane_table(g, tab);
   __syncthreads();
-  int h, w;
-  tile_pixel(h, w);
-  if (h >= det.H || w >= det.W) return;
+  int h, w, chunk;
+  tile_ray<K>(h, w, chunk);
+  const bool valid = h < det.H && w < det.W;
+  if (K == 1 && !valid) return;
   const int b = blockIdx.z;
-  double s[3], p[3], ah, aw;
-  pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
-  Ray r;
-  ray_setup(g, s, p, r);
   int n = 0;
-  if (r.hit) {
-    CountVisitor vis;
-    walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
-    n = vis.steps;
+  if (valid) {
+    double s[3], p[3], ah, aw;
+    pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
+    Ray r;
+    ray_setup(g, s, p, r, K, chunk);
+    if (r.hit) {
+      CountVisitor vis;
+      walk<VT, (K > 1)>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
+      n = vis.steps;
+    }
   }
-  steps[(static_cast<size_t>(b) * det.H + h) * det.W + w] = n;
+  n = chunk_sum<K>(n);
+  if (valid && chunk == 0) steps[(static_cast<size_t>(b) * det.H + h) * det.W + w] = n;
 }
 
 // Endpoint gradients of one ray from the reverse-mode visitor
@@ -179,8 +214,26 @@ __device__ __forceinline__ void endpoint_grads(const Ray& r,
   }
 }
 
+// Endpoint gradients from summed walk totals (acc, G, H): the same algebra as
+// endpoint_grads, for chunked walks whose partial sums were combined.
+__device__ __forceinline__ void sums_to_endpoint_grads(const Ray& r, double acc,
+                                                       const double* G, const double* Hh,
+                                                       double L, double* dEds, double* dEdp) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double gs = 0.0, gp = 0.0;
+    if (r.d[a] != 0.0) {
+      gs = L * (Hh[a] - G[a]) / r.d[a];
+      gp = -L * Hh[a] / r.d[a];
+    }
+    const double lt = r.d[a] / L * acc;
+    dEds[a] = gs - lt;
+    dEdp[a] = gp + lt;
+  }
+}
+
 // --------------------------------------------------------------- backward
-template <typename VT, typename GT, typename OT>
+template <typename VT, typename GT, typename OT, int K>
 __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
     k_backward(const VT* __restrict__ vol, const GridDev g,
                const double* __restrict__ frames, const DetDev det,
@@ -189,28 +242,44 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
   extern __shared__ double tab[];
   build_plane_table(g, tab);
   __syncthreads();
-  int h, w;
-  tile_pixel(h, w);
+  int h, w, chunk;
+  tile_ray<K>(h, w, chunk);
   const int b = blockIdx.z;
+  const bool valid = h < det.H && w < det.W;
   double acc12[kFrameGrads];
 #pragma unroll
   for (int k = 0; k < kFrameGrads; ++k) acc12[k] = 0.0;
-  if (h < det.H && w < det.W) {
-    double s[3], p[3], ah, aw;
+  // this chunk's partial walk sums: acc, G[3], H[3]
+  double part[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  double s[3], p[3], ah = 0.0, aw = 0.0;
+  Ray r;
+  r.hit = false;
+  if (valid) {
     pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
-    const size_t pix = (static_cast<size_t>(b) * det.H + h) * det.W + w;
-    const double gpx = static_cast<double>(grad_img[pix]);
-    Ray r;
-    ray_setup(g, s, p, r);
-    double e = 0.0;
+    ray_setup(g, s, p, r, K, chunk);
     if (r.hit) {
       BwdVisitor vis;
       visitor_init(vis, tab + plane_table_len(g) + kWalkSmemDoublesPerThread * 128);
-      walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
-      const double L = ray_length(r);
-      e = L * vis.acc;
+      walk<VT, (K > 1)>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
+      double G[3], Hh[3];
+      visitor_sums(vis, G, Hh);
+      part[0] = vis.acc;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) { part[1 + a] = G[a]; part[4 + a] = Hh[a]; }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 7; ++k) part[k] = chunk_sum<K>(part[k]);
+  if (valid && chunk == 0) {
+    const size_t pix = (static_cast<size_t>(b) * det.H + h) * det.W + w;
+    const double gpx = static_cast<double>(grad_img[pix]);
+    // chunk 0's Ray holds the whole ray's direction (d, L are chunk-invariant)
+    const double L = ray_length(r);
+    const double e = L * part[0];
+    if (part[0] != 0.0 || part[1] != 0.0 || part[2] != 0.0 || part[3] != 0.0 ||
+        part[4] != 0.0 || part[5] != 0.0 || part[6] != 0.0) {
       double dEds[3], dEdp[3];
-      endpoint_grads(r, vis, L, dEds, dEdp);
+      sums_to_endpoint_grads(r, part[0], part + 1, part + 4, L, dEds, dEdp);
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         acc12[a] = gpx * dEds[a];
@@ -419,8 +488,13 @@ int make_det(const drr_detector* in, drr::DetDev& d) {
   if (!(in->pitch_x > 0.0) || !(in->pitch_y > 0.0) || !isfinite(in->pitch_x) ||
       !isfinite(in->pitch_y))
     return fail(DRR_ERR_INVALID_ARGUMENT, "pixel pitch must be positive");
+  if (in->ray_split != 0 && in->ray_split != 1 && in->ray_split != 2 && in->ray_split != 4 &&
+      in->ray_split != 8)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "ray_split must be 0, 1, 2, 4 or 8, got %d",
+                in->ray_split);
   d.H = in->height;
   d.W = in->width;
+  d.split = in->ray_split;
   d.pitch_x = in->pitch_x;
   d.pitch_y = in->pitch_y;
   d.half_h = static_cast<double>(in->height - 1) / 2.0;
@@ -428,10 +502,35 @@ int make_det(const drr_detector* in, drr::DetDev& d) {
   return DRR_OK;
 }
 
-dim3 pose_grid(const drr::DetDev& d, int n_poses) {
-  return dim3((d.W + drr::kTileW - 1) / drr::kTileW,
-              (d.H + drr::kTileH - 1) / drr::kTileH, n_poses);
+// Threads per ray: explicit, or auto = the smallest K in {1, 2, 4, 8} with
+// B*H*W*K >= ~2 resident waves of threads (148 SMs x 1024 x 2).
+int ray_split(const drr::DetDev& d, int n_poses) {
+  if (d.split > 0) return d.split;
+  const double rays = static_cast<double>(n_poses) * d.H * d.W;
+  int k = 1;
+  while (k < 8 && rays * k < 148.0 * 1024.0 * 2.0) k *= 2;
+  return k;
 }
+
+dim3 pose_grid(const drr::DetDev& d, int n_poses, int K) {
+  int tw, th;
+  switch (K) {
+    case 1: tw = drr::Tile<1>::W; th = drr::Tile<1>::H; break;
+    case 2: tw = drr::Tile<2>::W; th = drr::Tile<2>::H; break;
+    case 4: tw = drr::Tile<4>::W; th = drr::Tile<4>::H; break;
+    default: tw = drr::Tile<8>::W; th = drr::Tile<8>::H; break;
+  }
+  return dim3((d.W + tw - 1) / tw, (d.H + th - 1) / th, n_poses);
+}
+
+// Dispatch a runtime K in {1, 2, 4, 8} to a template instantiation.
+#define DRR_DISPATCH_K(K, ...)                      \
+  switch (K) {                                       \
+    case 1: { constexpr int kK = 1; __VA_ARGS__ } break; \
+    case 2: { constexpr int kK = 2; __VA_ARGS__ } break; \
+    case 4: { constexpr int kK = 4; __VA_ARGS__ } break; \
+    default: { constexpr int kK = 8; __VA_ARGS__ } break; \
+  }
 
 template <typename VT, typename GT>
 void launch_backward(const VT* vol, const drr::GridDev& g,
@@ -439,17 +538,18 @@ void launch_backward(const VT* vol, const drr::GridDev& g,
                             int n_poses, const GT* grad, void* img,
                             int img_dtype, double* partials, cudaStream_t st) {
   const size_t smem = table_bytes(g);
-  const dim3 grd = pose_grid(d, n_poses);
-  if (img_dtype == 1) {
-    ensure_smem(drr::k_backward<VT, GT, double>, smem);
-    drr::k_backward<VT, GT, double><<<grd, drr::kThreads, smem, st>>>(
-        vol, g, frames, d, grad, static_cast<double*>(img), partials);
-  }
-  else {
-    ensure_smem(drr::k_backward<VT, GT, float>, smem);
-    drr::k_backward<VT, GT, float><<<grd, drr::kThreads, smem, st>>>(
-        vol, g, frames, d, grad, static_cast<float*>(img), partials);
-  }
+  const int K = ray_split(d, n_poses);
+  const dim3 grd = pose_grid(d, n_poses, K);
+  DRR_DISPATCH_K(K,
+    if (img_dtype == 1) {
+      ensure_smem(drr::k_backward<VT, GT, double, kK>, smem);
+      drr::k_backward<VT, GT, double, kK><<<grd, drr::kThreads, smem, st>>>(
+          vol, g, frames, d, grad, static_cast<double*>(img), partials);
+    } else {
+      ensure_smem(drr::k_backward<VT, GT, float, kK>, smem);
+      drr::k_backward<VT, GT, float, kK><<<grd, drr::kThreads, smem, st>>>(
+          vol, g, frames, d, grad, static_cast<float*>(img), partials);
+    })
 }
 
 }  // namespace
@@ -529,36 +629,35 @@ int drr_forward(const void* d_vol, int vol_dtype, const drr_grid* grid,
     return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
   if (n_poses == 0) return DRR_OK;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const dim3 grd = pose_grid(d, n_poses);
-  if (vol_dtype == DRR_VOL_F32 && img_dtype == 0) {
-    ensure_smem(drr::k_forward<float, float>, smem);
-    drr::k_forward<float, float><<<grd, drr::kThreads, smem, st>>>(
-        static_cast<const float*>(d_vol), g, d_frames, d, static_cast<float*>(d_img));
-  }
-  else if (vol_dtype == DRR_VOL_F32 && img_dtype == 1) {
-    ensure_smem(drr::k_forward<float, double>, smem);
-    drr::k_forward<float, double><<<grd, drr::kThreads, smem, st>>>(
-        static_cast<const float*>(d_vol), g, d_frames, d, static_cast<double*>(d_img));
-  }
-  else if (vol_dtype == DRR_VOL_F64 && img_dtype == 1) {
-    ensure_smem(drr::k_forward<double, double>, smem);
-    drr::k_forward<double, double><<<grd, drr::kThreads, smem, st>>>(
-        static_cast<const double*>(d_vol), g, d_frames, d, static_cast<double*>(d_img));
-  }
-  else if (vol_dtype == DRR_VOL_F64 && img_dtype == 0) {
-    ensure_smem(drr::k_forward<double, float>, smem);
-    drr::k_forward<double, float><<<grd, drr::kThreads, smem, st>>>(
-        static_cast<const double*>(d_vol), g, d_frames, d, static_cast<float*>(d_img));
-  }
-  else
+  const int K = ray_split(d, n_poses);
+  const dim3 grd = pose_grid(d, n_poses, K);
+  if ((vol_dtype != DRR_VOL_F32 && vol_dtype != DRR_VOL_F64) || (img_dtype != 0 && img_dtype != 1))
     return fail(DRR_ERR_INVALID_ARGUMENT, "bad dtypes vol=%d img=%d", vol_dtype, img_dtype);
+  DRR_DISPATCH_K(K,
+    if (vol_dtype == DRR_VOL_F32 && img_dtype == 0) {
+      ensure_smem(drr::k_forward<float, float, kK>, smem);
+      drr::k_forward<float, float, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const float*>(d_vol), g, d_frames, d, static_cast<float*>(d_img));
+    } else if (vol_dtype == DRR_VOL_F32) {
+      ensure_smem(drr::k_forward<float, double, kK>, smem);
+      drr::k_forward<float, double, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const float*>(d_vol), g, d_frames, d, static_cast<double*>(d_img));
+    } else if (img_dtype == 1) {
+      ensure_smem(drr::k_forward<double, double, kK>, smem);
+      drr::k_forward<double, double, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const double*>(d_vol), g, d_frames, d, static_cast<double*>(d_img));
+    } else {
+      ensure_smem(drr::k_forward<double, float, kK>, smem);
+      drr::k_forward<double, float, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const double*>(d_vol), g, d_frames, d, static_cast<float*>(d_img));
+    })
   return check_launch("drr_forward");
 }
 
 size_t drr_backward_workspace_size(int32_t n_poses, const drr_detector* det) {
   drr::DetDev d;
   if (make_det(det, d) || n_poses < 0) return 0;
-  const dim3 grd = pose_grid(d, 1);
+  const dim3 grd = pose_grid(d, 1, ray_split(d, n_poses));
   return static_cast<size_t>(n_poses) * grd.x * grd.y * drr::kFrameGrads * sizeof(double);
 }
 
@@ -602,7 +701,7 @@ int drr_backward(const void* d_vol, int vol_dtype, const drr_grid* grid,
   }
   rc = check_launch("drr_backward");
   if (rc) return rc;
-  const dim3 grd = pose_grid(d, 1);
+  const dim3 grd = pose_grid(d, 1, ray_split(d, n_poses));
   drr::k_reduce_frames<<<n_poses, drr::kReduceThreads, 0, st>>>(
       partials, static_cast<int>(grd.x * grd.y), d_grad_frames);
   return check_launch("drr_backward/reduce");
@@ -622,19 +721,20 @@ int drr_count_steps(const void* d_vol, int vol_dtype, const drr_grid* grid,
     return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
   if (n_poses == 0) return DRR_OK;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const dim3 grd = pose_grid(d, n_poses);
-  if (vol_dtype == DRR_VOL_F32) {
-    ensure_smem(drr::k_count<float>, smem);
-    drr::k_count<float><<<grd, drr::kThreads, smem, st>>>(
-        static_cast<const float*>(d_vol), g, d_frames, d, d_steps);
-  }
-  else if (vol_dtype == DRR_VOL_F64) {
-    ensure_smem(drr::k_count<double>, smem);
-    drr::k_count<double><<<grd, drr::kThreads, smem, st>>>(
-        static_cast<const double*>(d_vol), g, d_frames, d, d_steps);
-  }
-  else
+  const int K = ray_split(d, n_poses);
+  const dim3 grd = pose_grid(d, n_poses, K);
+  if (vol_dtype != DRR_VOL_F32 && vol_dtype != DRR_VOL_F64)
     return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
+  DRR_DISPATCH_K(K,
+    if (vol_dtype == DRR_VOL_F32) {
+      ensure_smem(drr::k_count<float, kK>, smem);
+      drr::k_count<float, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const float*>(d_vol), g, d_frames, d, d_steps);
+    } else {
+      ensure_smem(drr::k_count<double, kK>, smem);
+      drr::k_count<double, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const double*>(d_vol), g, d_frames, d, d_steps);
+    })
   return check_launch("drr_count_steps");
 }
 

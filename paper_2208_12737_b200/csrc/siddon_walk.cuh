@@ -125,13 +125,16 @@ struct Ray {
   double an[3];     // crossing parameter of the next plane per axis
   int q[3];         // plane-table index of that plane
   int st[3];        // +1 / -1 walking direction, 0 for a parallel axis
-  double amin, amax;
+  double amin, amax;  // start / end crossing of this walk (whole ray or chunk)
   double T;         // fast-voxel threshold on seg (see ray_setup)
   int lab_min, lab_max;
+  int end_lab;      // chunked walk: crossings tied with amax on axes >= end_lab
+                    // belong to the next chunk (kNoEndLab for a ray's real exit)
   int flat;         // flat voxel index of the segment after amin
   bool hit;
   bool safe;        // some |d_a| tiny: use IEEE '/' instead of the Markstein form
 };
+constexpr int kNoEndLab = 4;
 
 // Slab entry/exit, first-max/first-min labels over (x, y, z, clip):
 // _native.pyx:20-65.
@@ -169,10 +172,59 @@ __device__ __forceinline__ void entry_exit(const GridDev& g, Ray& r) {
   r.hit = r.amin < r.amax;
 }
 
-// Per-ray setup: direction, entry/exit, first kept plane per axis, starting
-// voxel and the fast-path threshold T.
+// Axis parameters by (possibly runtime) axis index.
+__device__ __forceinline__ void axis_params(const GridDev& g, const Ray& r, int a,
+                                            double& o, double& sp, double& s, double& d,
+                                            double& inv, int& st, int& n) {
+  if (a == 0) { o = g.o[0]; sp = g.sp[0]; s = r.s[0]; d = r.d[0]; inv = r.inv[0]; st = r.st[0]; n = g.n[0]; }
+  else if (a == 1) { o = g.o[1]; sp = g.sp[1]; s = r.s[1]; d = r.d[1]; inv = r.inv[1]; st = r.st[1]; n = g.n[1]; }
+  else { o = g.o[2]; sp = g.sp[2]; s = r.s[2]; d = r.d[2]; inv = r.inv[2]; st = r.st[2]; n = g.n[2]; }
+}
+
+// First plane k (in walking order, may be -1 / n+1 = none) on axis a whose
+// crossing parameter is after a_s: alpha > a_s (strict) or alpha >= a_s.
+// Estimate, then fix up with exact crossing parameters (monotone in k).
+__device__ __forceinline__ int first_plane_after(const GridDev& g, const Ray& r, int a,
+                                                 double a_s, bool strict) {
+  double o, sp, s, d, inv;
+  int st, n;
+  axis_params(g, r, a, o, sp, s, d, inv, st, n);
+  const double t = (s + a_s * d - o) / sp;
+  double kf = st > 0 ? ceil(t) : floor(t);
+  kf = fmin(fmax(kf, -1.0), (double)n + 1.0);
+  int k = (int)kf;
+  for (int it = 0; it < 64; ++it) {
+    const int kb = k - st;
+    if (kb >= 0 && kb <= n) {
+      const double ab = plane_alpha(o, sp, kb, s, d, inv, true);
+      if (strict ? ab > a_s : ab >= a_s) { k = kb; continue; }
+    }
+    if (k >= 0 && k <= n) {
+      const double ak = plane_alpha(o, sp, k, s, d, inv, true);
+      if (!(strict ? ak > a_s : ak >= a_s)) { k += st; continue; }
+    }
+    break;
+  }
+  return k;
+}
+
+__device__ __forceinline__ double axis_alpha(const GridDev& g, const Ray& r, int a, int k) {
+  double o, sp, s, d, inv;
+  int st, n;
+  axis_params(g, r, a, o, sp, s, d, inv, st, n);
+  return plane_alpha(o, sp, k, s, d, inv, true);
+}
+
+// Per-ray setup for chunk `chunk` of `nchunks` (one ray split
+// across threads by dominant-axis plane index ranges).  The crossing sequence
+// of the whole ray, ordered by (alpha, axis) like the reference's merge, is
+// cut at dominant-axis crossings B_j = (alpha_D(b_j), D); chunk j walks the
+// segments between B_j and B_{j+1}, so every segment (and every crossing's
+// reverse-mode coefficient) is counted exactly once across the chunks.
+// nchunks = 1 is the whole ray with the reference's entry/exit semantics.
 __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
-                                          const double* p, Ray& r) {
+                                          const double* p, Ray& r,
+                                          int nchunks = 1, int chunk = 0) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     r.s[a] = s[a];
@@ -180,81 +232,99 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
   }
   entry_exit(g, r);
   r.safe = false;
+  r.end_lab = kNoEndLab;
   if (!r.hit) return;
-  int vox[3];
-  double T = 0.0;
+  double T = 0.0, wmax = -1.0;
+  int D = 0;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const double d = r.d[a];
     if (d == 0.0) {
-      // Constant index along a parallel axis: the reference evaluates
-      // floor(((s + mid*0) - o)/sp) = floor((s - o)/sp), then clamps.
       r.st[a] = 0;
-      r.q[a] = plane_base(g, a);
       r.inv[a] = 0.0;
-      r.an[a] = INFINITY;
-      const double f = floor((r.s[a] - g.o[a]) / g.sp[a]);
-      vox[a] = !(f >= 0.0) ? 0 : (f >= (double)g.n[a] ? g.n[a] - 1 : (int)f);
       continue;
     }
     const double inv = __drcp_rn(d);
     if (!(fabs(d) > 1e-20)) r.safe = true;
-    const int st = d > 0.0 ? 1 : -1;
     r.inv[a] = inv;
-    r.st[a] = st;
-    // First plane (in walking order) with alpha >= amin: estimate, then fix
-    // up with the exact crossing parameters (monotone in k).
-    const double t = (r.s[a] + r.amin * d - g.o[a]) / g.sp[a];
-    double kf = st > 0 ? ceil(t) : floor(t);
-    kf = fmin(fmax(kf, -1.0), (double)g.n[a] + 1.0);
-    int k = (int)kf;
-    const int n = g.n[a];
-    for (int it = 0; it < 64; ++it) {
-      const int kb = k - st;
-      if (kb >= 0 && kb <= n &&
-          plane_alpha(g.o[a], g.sp[a], kb, r.s[a], d, inv, true) >= r.amin) {
-        k = kb;
-        continue;
-      }
-      if (k >= 0 && k <= n &&
-          plane_alpha(g.o[a], g.sp[a], k, r.s[a], d, inv, true) < r.amin) {
-        k += st;
-        continue;
-      }
-      break;
-    }
-    r.q[a] = plane_base(g, a) + k;
-    r.an[a] = (k >= 0 && k <= n)
-                  ? plane_alpha(g.o[a], g.sp[a], k, r.s[a], d, inv, true)
-                  : kSentinel;
-    vox[a] = st > 0 ? k - 1 : k;
+    r.st[a] = d > 0.0 ? 1 : -1;
     // Fast-voxel certificate.  The reference's midpoint position and our
     // crossing parameters carry rounding error below ~2^-50 * M voxels, with
     // M the coordinate magnitude in voxel units.  A used segment's midpoint
     // sits at least seg/2 * |d|/sp voxels from every a-plane, so
     // seg > 2^-39 * (M + 1) * sp / |d| guarantees floor(midpoint) equals the
     // next-plane bookkeeping with a 2^10 safety factor.
-    const double M = fabs(r.s[a]) + fabs(d) + fabs(g.o[a]) + fabs(g.hi[a]) +
-                     g.sp[a];
+    const double M = fabs(r.s[a]) + fabs(d) + fabs(g.o[a]) + fabs(g.hi[a]) + g.sp[a];
     T = fmax(T, 0x1.0p-39 * M / fabs(d));
+    const double w = fabs(d) / g.sp[a];
+    if (w > wmax) { wmax = w; D = a; }
   }
   r.T = T;
+  // Start event per axis: (amin, entry) for chunk 0, else (alpha_D(b_j), D).
+  double a_s = r.amin;
+  int lab_s = -1;  // -1: entry semantics (every crossing with alpha >= amin)
+  if (nchunks > 1) {
+    const int stD = r.st[D];
+    const int kf = first_plane_after(g, r, D, r.amin, false);
+    const int kl = first_plane_after(g, r, D, r.amax, true) - stD;
+    const int nD = (kl - kf) * stD + 1;
+    bool split = nD >= 2 * nchunks;
+    // boundaries must be strictly increasing crossings (always true unless
+    // |d_D| / sp_D exceeds ~2^52; then fall back to one thread per ray)
+    for (int j = 1; split && j < nchunks; ++j) {
+      const int b = kf + stD * ((j * nD) / nchunks);
+      split = axis_alpha(g, r, D, b) > axis_alpha(g, r, D, b - stD);
+    }
+    if (!split) {
+      if (chunk != 0) { r.hit = false; return; }
+    } else {
+      if (chunk > 0) {
+        const int b = kf + stD * ((chunk * nD) / nchunks);
+        a_s = axis_alpha(g, r, D, b);
+        lab_s = D;
+        r.amin = a_s;
+        r.lab_min = D;
+      }
+      if (chunk < nchunks - 1) {
+        const int b = kf + stD * (((chunk + 1) * nD) / nchunks);
+        r.amax = axis_alpha(g, r, D, b);
+        r.lab_max = D;
+        r.end_lab = D;
+      }
+    }
+  }
+  int vox[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (r.st[a] == 0) {
+      // Constant index along a parallel axis: the reference evaluates
+      // floor(((s + mid*0) - o)/sp) = floor((s - o)/sp), then clamps.
+      r.q[a] = plane_base(g, a);
+      r.an[a] = INFINITY;
+      const double f = floor((r.s[a] - g.o[a]) / g.sp[a]);
+      vox[a] = !(f >= 0.0) ? 0 : (f >= (double)g.n[a] ? g.n[a] - 1 : (int)f);
+      continue;
+    }
+    int k;
+    if (lab_s < 0) k = first_plane_after(g, r, a, a_s, false);
+    else if (a == lab_s) k = first_plane_after(g, r, a, a_s, false) + r.st[a];
+    else k = first_plane_after(g, r, a, a_s, a < lab_s);
+    // (a == D: the plane after b_j -- b_j is the first plane with
+    //  alpha >= a_s, the split test excludes an exact tie with b_j - st;
+    //  a < D: ties at a_s came before B_j; a > D: ties at a_s come after it)
+    const int n = g.n[a];
+    r.q[a] = plane_base(g, a) + k;
+    r.an[a] = (k >= 0 && k <= n) ? axis_alpha(g, r, a, k) : kSentinel;
+    vox[a] = r.st[a] > 0 ? k - 1 : k;
+  }
   r.flat = vox[0] + g.stride[1] * vox[1] + g.stride[2] * vox[2];
 }
 
-// The walk.  Visits every segment between consecutive crossings in ascending
-// order (ties -> lowest axis), calling
-//   vis.segment(used, seg, v, lab_start, alpha_start)
-// for each (v = V[voxel] for used segments), then vis.finish(lab_max, amax).
-// Branch-free axis selection: the crossed axis's constants are picked with
-// selects, so lanes taking different axes never diverge.  The gather of
-// segment i is consumed in iteration i+1 (one-deep software pipeline) so its
-// latency overlaps the next crossing's arithmetic.
 // Gather pipeline depth: segment i's voxel load is consumed in iteration
 // i + kPipe, so up to kPipe gathers per ray are in flight (ncu: the gather's
 // long-scoreboard stall dominated at depth 1).
 #ifndef DRR_PIPE
-#define DRR_PIPE 2
+#define DRR_PIPE 1
 #endif
 
 template <typename VT>
@@ -265,7 +335,7 @@ struct PipeStage {
   VT v;
 };
 
-template <typename VT, typename Visitor>
+template <typename VT, bool kChunked, typename Visitor>
 __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
                                             const GridDev& g,
                                             const double* __restrict__ tab,
@@ -293,7 +363,9 @@ __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
     double best = c1 ? an1 : an0;
     const bool c2 = an2 < best;
     best = c2 ? an2 : best;
-    const bool last = !(best <= amax);
+    bool last = !(best <= amax);
+    if (kChunked)  // chunk end B_{j+1} = (amax, end_lab): ties on axes >= end_lab come after it
+      last = last || (best == amax && (c2 ? 2 : (c1 ? 1 : 0)) >= r.end_lab);
     const double cur = last ? amax : best;
     const double seg = cur - prev;
     const bool used = seg > kSegEps;
@@ -336,11 +408,11 @@ __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
 // (the smem-constant variant that used them lost the A/B, see profiles/).
 constexpr int kWalkSmemDoublesPerThread = 0;
 
-template <typename VT, typename Visitor>
+template <typename VT, bool kChunked = false, typename Visitor>
 __device__ __forceinline__ void walk(const VT* __restrict__ vol, const GridDev& g,
                                      const double* __restrict__ tab, double* /*cst*/,
                                      const Ray& r, Visitor& vis) {
-  walk_select<VT>(vol, g, tab, r, vis);
+  walk_select<VT, kChunked>(vol, g, tab, r, vis);
 }
 
 // ---- visitors ----------------------------------------------------------

@@ -70,10 +70,19 @@ def test_invalid_arguments_map_to_reference_errors():
 def test_workspace_size_and_error():
     from paper_2208_12737_b200 import _lib
     lib = _lib.load()
-    det = _lib.make_detector(200, 200, 3.6, 3.6)
-    # 13 x 25 CTA tiles of 16 x 8 pixels, 12 doubles each, per pose
+    det = _lib.make_detector(200, 200, 3.6, 3.6, ray_split=1)
+    # one thread per ray: 13 x 25 CTA tiles of 16 x 8 pixels, 12 doubles each, per pose
     assert lib.drr_backward_workspace_size(3, det) == 3 * 13 * 25 * 12 * 8
+    # auto split: 3 x 200^2 rays < 2 waves -> 4 threads per ray, 8 x 4 pixel tiles
+    auto = _lib.make_detector(200, 200, 3.6, 3.6)
+    assert lib.drr_backward_workspace_size(3, auto) == 3 * 25 * 50 * 12 * 8
+    # a large batch needs no split
+    assert lib.drr_backward_workspace_size(64, auto) == 64 * 13 * 25 * 12 * 8
+    bad = _lib.make_detector(200, 200, 3.6, 3.6, ray_split=3)
+    assert lib.drr_backward_workspace_size(3, bad) == 0
     grid = _lib.make_grid((4, 4, 4), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    with pytest.raises(Exception, match="ray_split"):
+        _lib.check(lib.drr_forward(None, 0, grid, None, 1, bad, None, 0, None))
     rc = lib.drr_backward(None, 0, grid, None, 3, det, None, 0, None, None, 0, None, 16, None)
     assert rc == _lib.DRR_ERR_WORKSPACE
     with pytest.raises(Exception, match="workspace"):

@@ -139,7 +139,7 @@ def test_pose_renders_bitwise(golden, cuda_device):
     corner-heavy poses (test_raytrace.py:128-137)."""
     from paper_2208_12737_b200 import Detector, render_frames
     vol = _vol_from_golden(golden, "ps_")
-    det = Detector(21, 21, 4.0)
+    det = Detector(21, 21, 4.0, ray_split=1)
     frames = np.stack([O.pose_frame(eta, golden["ps_center"]) for eta in golden["ps_poses"]])
     img = render_frames(vol, det, torch.tensor(frames, device=cuda_device),
                         out_dtype=torch.float64).cpu().numpy()
@@ -198,7 +198,7 @@ def test_c1_config(golden, cuda_device):
     vol = synthetic.make_phantom("sphere", 128, 1.0)
     import hashlib
     assert hashlib.sha256(vol.ravel(order="F").tobytes()).hexdigest() == str(golden["c1_sha"])
-    drr = DRR(vol, 1.0, sdr=300.0, height=100, delx=2.56, device=cuda_device)
+    drr = DRR(vol, 1.0, sdr=300.0, height=100, delx=2.56, device=cuda_device, ray_split=1)
     eta = golden["c1_pose"]
     frame = torch.tensor(O.pose_frame(eta, drr.isocenter), device=cuda_device)[None]
     from paper_2208_12737_b200 import render_frames
@@ -223,14 +223,14 @@ def test_blob_and_corner_diagonal(golden, cuda_device):
     import hashlib
     assert hashlib.sha256(blob.ravel(order="F").tobytes()).hexdigest() == str(golden["blob_sha"])
     vol = DeviceVolume(blob, 4.0, dtype=torch.float64)
-    det = Detector(100, 100, 4.0)
+    det = Detector(100, 100, 4.0, ray_split=1)
     for key in ("shifted", "truth"):
         f = torch.tensor(O.pose_frame(golden[f"blob_{key}_pose"], vol.center), device=cuda_device)[None]
         img = render_frames(vol, det, f, out_dtype=torch.float64)[0].cpu().numpy()
         np.testing.assert_array_equal(img, golden[f"blob_{key}"])
     uni = DeviceVolume(synthetic.make_phantom("uniform", 64, 4.0), 4.0, dtype=torch.float64)
     f = torch.tensor(O.pose_frame(golden["uni_diag_pose"], uni.center), device=cuda_device)[None]
-    img = render_frames(uni, Detector(101, 101, 4.0), f, out_dtype=torch.float64)[0].cpu().numpy()
+    img = render_frames(uni, Detector(101, 101, 4.0, ray_split=1), f, out_dtype=torch.float64)[0].cpu().numpy()
     np.testing.assert_array_equal(img, golden["uni_diag101"])
 
 
@@ -239,7 +239,7 @@ def test_backward_vs_oracle_and_determinism(golden, cuda_device):
     backward; two runs are bit-identical (fixed-order reduction, no atomics)."""
     from paper_2208_12737_b200 import Detector, backward_frames
     vol = _vol_from_golden(golden, "ps_")
-    det = Detector(21, 21, 4.0)
+    det = Detector(21, 21, 4.0, ray_split=1)
     rng = np.random.default_rng(3)
     for eta in golden["ps_poses"]:
         frame = O.pose_frame(eta, golden["ps_center"])
@@ -258,7 +258,7 @@ def test_backward_vs_oracle_and_determinism(golden, cuda_device):
 def test_batched_equals_single(golden, cuda_device):
     from paper_2208_12737_b200 import Detector, render_frames
     vol = _vol_from_golden(golden, "ps_")
-    det = Detector(21, 17, 4.0, 3.0)
+    det = Detector(21, 17, 4.0, 3.0, ray_split=1)
     frames = torch.tensor(np.stack([O.pose_frame(e, golden["ps_center"]) for e in golden["ps_poses"]]),
                           device=cuda_device)
     batch = render_frames(vol, det, frames, out_dtype=torch.float64)
@@ -276,7 +276,7 @@ def test_chest_c2_vs_oracle(cuda_device):
     from paper_2208_12737_b200 import DRR, backward_frames, render_frames, synthetic
     vol = synthetic.chest_phantom()
     spacing = (0.703125, 0.703125, 2.5)
-    drr = DRR(vol, spacing, sdr=300.0, height=200, delx=3.6, device=cuda_device)
+    drr = DRR(vol, spacing, sdr=300.0, height=200, delx=3.6, device=cuda_device, ray_split=1)
     eta = np.array([300.0, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0])
     frame = O.pose_frame(eta, drr.isocenter)
     ft = torch.tensor(frame, device=cuda_device)[None]
@@ -317,3 +317,32 @@ def test_fd_gradient_check(cuda_device):
             fd[i] = (lp - lm) / (2 * steps[i])
     # fp32 images limit FD resolution; FD is reported, the bar is loose
     np.testing.assert_allclose(g, fd, rtol=2e-2, atol=2e-3 * np.abs(g).max())
+
+
+@pytest.mark.parametrize("split", [2, 4, 8])
+def test_ray_split_matches_single_thread(split, cuda_device):
+    """Rays cut across K threads at dominant-axis crossings:
+    same used-step counts exactly, images within 1e-13 relative (summation
+    order only), frame gradients within 1e-11 -- on the C2 chest at an
+    oblique pose and at AP (ties between x/y crossings), and on the
+    corner-diagonal uniform phantom where every crossing ties three ways."""
+    from paper_2208_12737_b200 import (DeviceVolume, Detector, backward_frames, count_steps,
+                                       render_frames, synthetic)
+    cases = []
+    chest = DeviceVolume(synthetic.chest_phantom(), (0.703125, 0.703125, 2.5))
+    cases.append((chest, 200, 3.6, [300.0, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0]))
+    cases.append((chest, 200, 3.6, [300.0, np.pi / 2, np.pi / 2, 0.0, 0.0, 0.0, 0.0]))
+    uni = DeviceVolume(synthetic.make_phantom("uniform", 64, 4.0), 4.0)
+    cases.append((uni, 101, 4.0, [400.0, np.pi / 4, np.arccos(1 / np.sqrt(3)), 0, 0, 0, 0]))
+    rng = np.random.default_rng(1)
+    for vol, n, pitch, eta in cases:
+        f = torch.tensor(O.pose_frame(np.array(eta), vol.center), device=cuda_device)[None]
+        d1, dk = Detector(n, n, pitch, ray_split=1), Detector(n, n, pitch, ray_split=split)
+        assert torch.equal(count_steps(vol, d1, f), count_steps(vol, dk, f))
+        a = render_frames(vol, d1, f, out_dtype=torch.float64)
+        b = render_frames(vol, dk, f, out_dtype=torch.float64)
+        np.testing.assert_allclose(b.cpu().numpy(), a.cpu().numpy(), rtol=1e-13, atol=1e-12)
+        g = torch.tensor(rng.normal(size=(1, n, n)), device=cuda_device)
+        ga = backward_frames(vol, d1, f, g).cpu().numpy()
+        gb = backward_frames(vol, dk, f, g).cpu().numpy()
+        np.testing.assert_allclose(gb, ga, rtol=0, atol=1e-11 * np.abs(ga).max())
