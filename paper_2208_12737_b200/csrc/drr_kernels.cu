@@ -44,6 +44,10 @@ namespace drr {
 #ifndef DRR_BWD_MINB
 #define DRR_BWD_MINB 5
 #endif
+// Forward: 8 CTAs/SM (<= 64 registers) -- ptxas picks 72 (7 CTAs) on its own.
+#ifndef DRR_FWD_MINB
+#define DRR_FWD_MINB 8
+#endif
 constexpr int kThreads = 128;  // 4 warps per CTA
 constexpr int kFrameGrads = 12;
 
@@ -116,7 +120,7 @@ __device__ __forceinline__ void store_out(OT* p, double v) {
 
 // ---------------------------------------------------------------- forward
 template <typename VT, typename OT, int K>
-__global__ void DRR_LB
+__global__ void __launch_bounds__(kThreads, DRR_FWD_MINB)
     k_forward(const VT* __restrict__ vol, const GridDev g,
               const double* __restrict__ frames, const DetDev det,
               OT* __restrict__ img) {
