@@ -44,7 +44,9 @@ namespace drr {
 #ifndef DRR_BWD_MINB
 #define DRR_BWD_MINB 5
 #endif
-// Forward: 8 CTAs/SM (<= 64 registers) -- ptxas picks 72 (7 CTAs) on its own.
+// Forward, one thread per ray: 8 CTAs/SM (<= 64 registers; ptxas alone picks
+// 72 = 7 CTAs): 2.84 vs 3.01 ms for 32 C2 poses.  Split rays (K > 1, few
+// rays) measured faster without the bound.
 #ifndef DRR_FWD_MINB
 #define DRR_FWD_MINB 8
 #endif
@@ -120,7 +122,7 @@ __device__ __forceinline__ void store_out(OT* p, double v) {
 
 // ---------------------------------------------------------------- forward
 template <typename VT, typename OT, int K>
-__global__ void __launch_bounds__(kThreads, DRR_FWD_MINB)
+__global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FWD_MINB : 1)
     k_forward(const VT* __restrict__ vol, const GridDev g,
               const double* __restrict__ frames, const DetDev det,
               OT* __restrict__ img) {
