@@ -336,6 +336,14 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None  # dram bytes per k_backward launch from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)["k_backward"]
+        if tr.get("poses") == B and tr.get("config") == "C2":
+            traffic = float(tr["traffic_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        pass
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     achieved_bwd = bytes_bwd / (bwd_ms / 1e3) / 1e9
 
@@ -388,7 +396,8 @@ def main():
                         "ms_per_step": module_ms, "value": B / (module_ms / 1e3)},
         "roofline": {"bound": "hbm", "kernel": "k_backward (fused re-walk + frame reduction)",
                      "achieved": achieved_bwd, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved_bwd / hbm_peak, "traffic": None,
+                     "frac": achieved_bwd / hbm_peak, "traffic": traffic,
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same kernel/config)",
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_bwd, "launch_ms": bwd_ms},
         "kernels": {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms,

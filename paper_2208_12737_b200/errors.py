@@ -28,3 +28,16 @@ class GradientUndefinedError(DrrTraceError):
 
 class KernelError(DrrTraceError, RuntimeError):
     """A CUDA launch or runtime failure inside the native library."""
+
+
+class HeaderParseError(DrrTraceError):
+    """A volume header could not be parsed (errors.py:12-20); ``offset`` is the
+    byte offset where parsing failed."""
+
+    def __init__(self, message, offset):
+        super().__init__(f"{message} (byte offset {offset})")
+        self.offset = offset
+
+
+class CorruptFileError(DrrTraceError):
+    """File contents disagree with the declared sizes (errors.py:23-24)."""

@@ -257,3 +257,86 @@ def register_batch(fixed_images, vol: DeviceVolume, poses0, det: Detector,
     eng.reset(poses0)
     eng.run(use_graph=use_graph)
     return eng.traces()
+
+
+# ---------------------------------------------------------------- landscape
+OPTIMIZED_PARAMS = ("theta", "phi", "gamma", "bx", "by", "bz")
+NARROW_HALF_WIDTHS = {"theta": math.radians(45.0), "phi": math.radians(45.0),
+                      "gamma": math.radians(22.5), "bx": 15.0, "by": 15.0, "bz": 15.0}
+
+
+@dataclass
+class LandscapeGrid:
+    """registration.py:150-156."""
+
+    axes: tuple
+    coords: tuple
+    losses: np.ndarray
+
+
+def loss_landscape(vol: DeviceVolume, det: Detector, truth, loss_kind: str = "neg_zncc",
+                   axes=("theta",), samples=41, half_widths=None, chunk: int = 1024,
+                   isocenter=None) -> LandscapeGrid:
+    """``registration.loss_landscape`` (registration.py:159-203) as batched
+    renders: the fixed image renders once at ``truth``; every grid pose is one
+    row of a (B, 7) batch -> drr_pose_frames -> drr_forward -> drr_image_loss
+    (value only), ``chunk`` poses per launch.  Undefined metrics give +inf."""
+    import ctypes
+    if isinstance(axes, str):
+        axes = (axes,)
+    axes = tuple(axes)
+    if not 1 <= len(axes) <= 2:
+        raise InvalidArgumentError(f"axes must name one or two parameters, got {axes}")
+    for name in axes:
+        if name not in OPTIMIZED_PARAMS:
+            raise InvalidArgumentError(f"unknown sweep axis {name!r}, expected one of {OPTIMIZED_PARAMS}")
+    if loss_kind not in LOSS_KINDS:
+        raise InvalidArgumentError(f"loss kind must be one of {tuple(LOSS_KINDS)}, got {loss_kind!r}")
+    samples = np.broadcast_to(np.asarray(samples, dtype=int), (len(axes),))
+    if np.any(samples < 3):
+        raise InvalidArgumentError(f"grid resolution must be >= 3 per axis, got {samples}")
+    if half_widths is None:
+        half_widths = [NARROW_HALF_WIDTHS[name] for name in axes]
+    half_widths = np.broadcast_to(np.asarray(half_widths, dtype=np.float64), (len(axes),))
+    center = np.asarray(truth, dtype=np.float64).reshape(7)
+    index = {name: i for i, name in enumerate(OPTIMIZED_PARAMS, start=1)}
+    coords = tuple(center[index[name]] + np.linspace(-hw, hw, int(ns))
+                   for name, hw, ns in zip(axes, half_widths, samples))
+    if len(axes) == 1:
+        grid = coords[0][:, None]
+    else:
+        grid = np.stack(np.meshgrid(coords[0], coords[1], indexing="ij"), -1).reshape(-1, 2)
+    etas = np.repeat(center[None], grid.shape[0], axis=0)
+    for j, name in enumerate(axes):
+        etas[:, index[name]] = grid[:, j]
+    dev = vol.device
+    lib = _lib.load()
+    st = _stream(dev)
+    iso = _iso(vol, isocenter)
+    npix = det.height * det.width
+    # fixed image at the truth pose
+    one = torch.tensor(center[None], device=dev)
+    fr = torch.empty((1, 12), dtype=torch.float64, device=dev)
+    fixed = torch.empty((1, det.height, det.width), dtype=torch.float32, device=dev)
+    _lib.check(lib.drr_pose_frames(one.data_ptr(), 1, iso, fr.data_ptr(), st))
+    _lib.check(lib.drr_forward(vol.flat.data_ptr(), vol.vol_dtype, vol.grid, fr.data_ptr(), 1,
+                               det.c, fixed.data_ptr(), 0, st))
+    out = torch.empty(etas.shape[0], dtype=torch.float64, device=dev)
+    status = torch.empty(etas.shape[0], dtype=torch.int32, device=dev)
+    all_eta = torch.tensor(etas, device=dev)
+    frames = torch.empty((min(chunk, etas.shape[0]), 12), dtype=torch.float64, device=dev)
+    img = torch.empty((min(chunk, etas.shape[0]), det.height, det.width), dtype=torch.float32,
+                      device=dev)
+    for s in range(0, etas.shape[0], chunk):
+        n = min(chunk, etas.shape[0] - s)
+        e = all_eta[s:s + n]
+        _lib.check(lib.drr_pose_frames(e.data_ptr(), n, iso, frames.data_ptr(), st))
+        _lib.check(lib.drr_forward(vol.flat.data_ptr(), vol.vol_dtype, vol.grid, frames.data_ptr(),
+                                   n, det.c, img.data_ptr(), 0, st))
+        _lib.check(lib.drr_image_loss(img.data_ptr(), fixed.data_ptr(), 0, 0, n, npix,
+                                      LOSS_KINDS[loss_kind], out[s:].data_ptr(), None,
+                                      status[s:].data_ptr(), st))
+    losses = torch.where(status != 0, torch.full_like(out, math.inf), out).cpu().numpy()
+    if len(axes) == 2:
+        losses = losses.reshape(len(coords[0]), len(coords[1]))
+    return LandscapeGrid(axes=axes, coords=coords, losses=losses)
