@@ -50,6 +50,9 @@ namespace drr {
 #ifndef DRR_FWD_MINB
 #define DRR_FWD_MINB 8
 #endif
+#ifndef DRR_SPLIT_MINB
+#define DRR_SPLIT_MINB 6
+#endif
 constexpr int kThreads = 128;  // 4 warps per CTA
 constexpr int kFrameGrads = 12;
 
@@ -122,7 +125,7 @@ __device__ __forceinline__ void store_out(OT* p, double v) {
 
 // ---------------------------------------------------------------- forward
 template <typename VT, typename OT, int K>
-__global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FWD_MINB : 1)
+__global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FWD_MINB : DRR_SPLIT_MINB)
     k_forward(const VT* __restrict__ vol, const GridDev g,
               const double* __restrict__ frames, const DetDev det,
               OT* __restrict__ img) {

@@ -264,7 +264,7 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
   double a_s = r.amin;
   int lab_s = -1;  // -1: entry semantics (every crossing with alpha >= amin)
   if (nchunks > 1) {
-    const int stD = r.st[D];
+    const int stD = D == 0 ? r.st[0] : (D == 1 ? r.st[1] : r.st[2]);
     const int kf = first_plane_after(g, r, D, r.amin, false);
     const int kl = first_plane_after(g, r, D, r.amax, true) - stD;
     const int nD = (kl - kf) * stD + 1;

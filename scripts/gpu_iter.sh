@@ -1,6 +1,6 @@
 # quick iteration: parity tests + kernel micro-bench (+ optional ncu of one kernel)
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q -rf --durations=8 > gpurun_out/pytest_gpu.txt 2>&1
 timeout 300 python scripts/kbench.py 32 1 > gpurun_out/kbench.json 2> gpurun_out/kbench.err
 timeout 300 python scripts/bench_registration.py 1 64 > gpurun_out/regbench.json 2> gpurun_out/regbench.err
 if [ -n "$NCU_KERNEL" ]; then
