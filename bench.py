@@ -2,9 +2,10 @@
 """Benchmark: DRRs/sec fwd+bwd (200x200 detector, 512x512x133 CT) on B200.
 
 One STEP = the hot path over one batch of poses: for B poses per GPU, render
-the 200x200 DRRs (drr_forward), evaluate the reference's registration loss
-(neg-ZNCC vs a fixed DRR, metrics.py:71-91) and back-propagate to the pose
-(drr_backward + autograd through the 12-number frame) -- i.e. B x the
+the 200x200 DRRs with each ray's Jacobian (drr_forward_jac: one CT walk),
+evaluate the reference's registration loss (neg-ZNCC vs a fixed DRR,
+metrics.py:71-91) and back-propagate to the pose (drr_backward_jac + the
+12-number frame chain) -- i.e. B x the
 reference's ``loss_and_gradient`` (gradients.py:61-69), config C2 of
 SURVEY.md 8(d) with the C4 pose sampling.  Poses shard across ranks with no
 collective in the loop (weak scaling); the CT is NCCL-broadcast once.
@@ -196,8 +197,9 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_2208_12737_b200 import (DRR, backward_frames, count_steps, pose_frames,
-                                       render_frames)
+    from paper_2208_12737_b200 import (DRR, backward_frames, backward_from_jac, count_steps,
+                                       pose_frames, render_frames, render_frames_jac)
+
     from paper_2208_12737_b200 import _lib
     from paper_2208_12737_b200.metrics import neg_zncc
 
@@ -236,11 +238,13 @@ def main():
     def step(eta):
         # the reference's unit of work, batched: loss_and_gradient
         # (gradients.py:61-69) = pose frames -> forward -> fused neg-ZNCC + pixel
-        # gradient -> fused backward re-walk -> pose gradient (6 native launches)
+        # gradient -> Jacobian contraction (+ fixed-order reduce) -> pose gradient
+        # (6 native launches; the CT is walked once per ray)
         return loss_and_gradient(drr.volume, drr.detector, eta, fixed, "neg_zncc", buffers=bufs)
 
     def module_step(rot, tra):
-        # the north-star nn.Module path (torch autograd around drr_forward/backward)
+        # the north-star nn.Module path (torch autograd around drr_forward_jac /
+        # drr_backward_jac)
         rot = rot.detach().requires_grad_(True)
         tra = tra.detach().requires_grad_(True)
         loss = neg_zncc(drr(rot, tra), fixed_b)
@@ -302,32 +306,37 @@ def main():
     rot0 = eta0[:, 1:4]
     tra0 = eta0[:, 4:7]
 
-    # --- roofline of the dominant kernel (k_backward) --------------------
+    # --- roofline of the dominant kernel (k_forward_jac: the only CT walk) --
     frames = pose_frames(drr.pose_vectors(rot0, tra0), drr.isocenter).detach()
     steps_used = count_steps(drr.volume, drr.detector, frames)
     S = float(steps_used.double().sum().item())  # used voxel-steps in the batch
     g_img = torch.randn((B, H, W), device=dev, dtype=torch.float32)
-    kt = {"bwd": [], "fwd": []}
+    kt = {"fj": [], "bj": [], "fwd": [], "rewalk": []}
+    jac_holder = {}
+
+    def k_fj():
+        jac_holder["img"], jac_holder["jac"] = render_frames_jac(drr.volume, drr.detector, frames)
+
+    kfns = {"fj": k_fj,
+            "bj": lambda: backward_from_jac(drr.detector, jac_holder["jac"], g_img),
+            "fwd": lambda: render_frames(drr.volume, drr.detector, frames),
+            "rewalk": lambda: backward_frames(drr.volume, drr.detector, frames, g_img)}
     for i in range(8):
-        flush.fill_(1.0)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        backward_frames(drr.volume, drr.detector, frames, g_img)
-        e1.record(stream)
-        flush.fill_(1.0)
-        e2 = torch.cuda.Event(enable_timing=True)
-        e3 = torch.cuda.Event(enable_timing=True)
-        e2.record(stream)
-        render_frames(drr.volume, drr.detector, frames)
-        e3.record(stream)
-        e3.synchronize()
-        if i >= 2:
-            kt["bwd"].append(e0.elapsed_time(e1))
-            kt["fwd"].append(e2.elapsed_time(e3))
-    bwd_ms = float(np.mean(kt["bwd"]))
-    fwd_ms = float(np.mean(kt["fwd"]))
-    bytes_bwd = 4.0 * S + 4.0 * B * H * W  # gathers + grad_img read
+        for name in ("fj", "bj", "fwd", "rewalk"):
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            kfns[name]()
+            e1.record(stream)
+            e1.synchronize()
+            if i >= 2:
+                kt[name].append(e0.elapsed_time(e1))
+    kms = {k: float(np.mean(v)) for k, v in kt.items()}
+    fj_ms = kms["fj"]
+    # algorithmic bytes per k_forward_jac launch: one fp32 gather per used
+    # voxel-step + fp32 image store + 6 f64 Jacobian entries per pixel
+    bytes_fj = 4.0 * S + 4.0 * B * H * W + 48.0 * B * H * W
     bytes_fwd = 4.0 * S + 4.0 * B * H * W  # gathers + image store
     peaks = {}
     try:
@@ -336,16 +345,16 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None  # dram bytes per k_backward launch from the committed ncu capture
+    traffic = None  # dram bytes per k_forward_jac launch from the committed ncu capture
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f)["k_backward"]
+            tr = json.load(f)["k_forward_jac"]
         if tr.get("poses") == B and tr.get("config") == "C2":
             traffic = float(tr["traffic_bytes_per_launch"])
     except (OSError, KeyError, ValueError):
         pass
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    achieved_bwd = bytes_bwd / (bwd_ms / 1e3) / 1e9
+    achieved_fj = bytes_fj / (fj_ms / 1e3) / 1e9
 
     # single-pose latency (C2 as configs[1] states it: one pose fwd+bwd)
     bufs1 = _Buffers(drr.volume, drr.detector, 1)
@@ -394,16 +403,19 @@ def main():
         "gpu_launches": 6 * args.steps,
         "module_path": {"api": "DRR nn.Module + torch neg_zncc + autograd",
                         "ms_per_step": module_ms, "value": B / (module_ms / 1e3)},
-        "roofline": {"bound": "hbm", "kernel": "k_backward (fused re-walk + frame reduction)",
-                     "achieved": achieved_bwd, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved_bwd / hbm_peak, "traffic": traffic,
+        "roofline": {"bound": "hbm",
+                     "kernel": "k_forward_jac (the one CT walk per step: image + ray Jacobian)",
+                     "achieved": achieved_fj, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved_fj / hbm_peak, "traffic": traffic,
                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same kernel/config)",
                      "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_bwd, "launch_ms": bwd_ms},
-        "kernels": {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+                     "algorithmic_bytes_per_launch": bytes_fj, "launch_ms": fj_ms},
+        "kernels": {"forward_jac_ms": fj_ms, "backward_jac_ms": kms["bj"],
+                    "forward_only_ms": kms["fwd"], "rewalk_backward_ms": kms["rewalk"],
                     "voxel_steps_per_drr": S / B,
-                    "voxel_steps_per_s_fwd": S / (fwd_ms / 1e3),
-                    "fwd_achieved_gbs": bytes_fwd / (fwd_ms / 1e3) / 1e9},
+                    "voxel_steps_per_s_forward_jac": S / (fj_ms / 1e3),
+                    "voxel_steps_per_s_forward_only": S / (kms["fwd"] / 1e3),
+                    "forward_only_achieved_gbs": bytes_fwd / (kms["fwd"] / 1e3) / 1e9},
         "single_pose_fwd_bwd_ms": float(np.mean(one)),
         "registration_c3": {"steps": reg_cfg.max_iters + 1, "ms_total": reg_ms,
                             "ms_per_step": reg_ms / (reg_cfg.max_iters + 1),

@@ -21,6 +21,11 @@
  *   drr_backward             <- gradients.py:45-69 render_with_gradient +
  *                               the pixel_grad @ d_image reduction, in reverse
  *                               mode down to the 12-number frame (s, c, e1, e2)
+ *   drr_forward_jac          <- gradients.py:45-58 render_with_gradient (image and
+ *                               per-ray derivatives from one walk, as
+ *                               _native.pyx:196-282 does)
+ *   drr_backward_jac         <- gradients.py:61-69 the pixel_grad @ d_image
+ *                               contraction, down to the 12-number frame
  *   drr_count_steps          <- _kernels/python_ref.py:191-201 ray_structure
  *                               (number of used voxel-steps per ray)
  *   drr_pose_frames          <- geometry.py:120-149 _pose_frame (+ the
@@ -115,6 +120,25 @@ int drr_backward(const void *d_vol, int vol_dtype, const drr_grid *grid,
                  int grad_dtype, double *d_grad_frames, void *d_img,
                  int img_dtype, void *d_workspace, size_t workspace_bytes,
                  void *stream);
+
+/* Forward with the ray Jacobian: ONE walk per ray writes the image (as
+ * drr_forward) and each ray's endpoint derivatives into d_jac, 6 x (B*H*W)
+ * float64 structure-of-arrays: rows 0-2 dE/ds, rows 3-5 dE/dp.  Replaces
+ * gradients.py:45-58 render_with_gradient, which also obtains energies and
+ * tangents from one traversal (_native.pyx:196-282 siddon_raysum_grad). */
+int drr_forward_jac(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                    const double *d_frames, int32_t n_poses,
+                    const drr_detector *det, void *d_img, int img_dtype,
+                    double *d_jac, void *stream);
+
+/* Backward from stored ray Jacobians (no walk): d_grad_frames (B x 12) =
+ * sum over pixels of grad_img * dE/d(s, c, e1, e2) in the same fixed order as
+ * drr_backward -- the `pixel_grad @ d_image` contraction of
+ * gradients.py:61-69.  Workspace: drr_backward_workspace_size. */
+int drr_backward_jac(const double *d_jac, int32_t n_poses,
+                     const drr_detector *det, const void *d_grad_img,
+                     int grad_dtype, double *d_grad_frames, void *d_workspace,
+                     size_t workspace_bytes, void *stream);
 
 /* Used voxel-steps per ray (segments longer than 1e-12), B x H x W int32. */
 int drr_count_steps(const void *d_vol, int vol_dtype, const drr_grid *grid,

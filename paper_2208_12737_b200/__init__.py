@@ -10,11 +10,12 @@ hand-written sm_100a CUDA behind the C ABI of ``include/drr_b200.h``.
 from .errors import (DegenerateRayError, DrrTraceError, GradientUndefinedError,
                      InvalidArgumentError, KernelError, MetricUndefinedError)
 from .geometry import POSE_PARAM_NAMES, pose_frames
-from .renderer import (DRR, DeviceVolume, Detector, backward_frames, count_steps,
-                       render_frames, render_pose_vectors)
+from .renderer import (DRR, DeviceVolume, Detector, backward_frames, backward_from_jac, count_steps,
+                       render_frames, render_frames_jac, render_pose_vectors)
 
 __all__ = [
     "DRR", "DeviceVolume", "Detector", "render_frames", "backward_frames",
+    "render_frames_jac", "backward_from_jac",
     "count_steps", "render_pose_vectors", "pose_frames", "POSE_PARAM_NAMES",
     "DrrTraceError", "InvalidArgumentError", "DegenerateRayError",
     "MetricUndefinedError", "GradientUndefinedError", "KernelError",

@@ -34,6 +34,8 @@ EXPORTS = (
     "drr_forward",
     "drr_backward_workspace_size",
     "drr_backward",
+    "drr_forward_jac",
+    "drr_backward_jac",
     "drr_count_steps",
     "drr_pose_frames",
     "drr_pose_grad",
@@ -80,6 +82,8 @@ _SIGNATURES = {
     "drr_forward": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp], _int),
     "drr_backward_workspace_size": ([_i32, _DP], _sz),
     "drr_backward": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp, _vp, _int, _vp, _sz, _vp], _int),
+    "drr_forward_jac": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp, _vp], _int),
+    "drr_backward_jac": ([_vp, _i32, _DP, _vp, _int, _vp, _vp, _sz, _vp], _int),
     "drr_count_steps": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
     "drr_pose_frames": ([_vp, _i32, ctypes.POINTER(ctypes.c_double), _vp, _vp], _int),
     "drr_pose_grad": ([_vp, _vp, _i32, _vp, _vp], _int),

@@ -326,6 +326,124 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
   }
 }
 
+// ------------------------------------------------- forward + ray Jacobian
+// One walk per ray yields the image AND the ray's endpoint derivatives
+// dE/ds, dE/dp (the reverse-mode form of siddon_raysum_grad's tangents,
+// _native.pyx:196-282): the reference's render_with_gradient also walks each
+// ray once for energies and tangents together (gradients.py:45-58).  The
+// pixel gradient is unknown until the loss has been evaluated, so the 6
+// derivatives are stored (SoA, jac[c * npix_total + pix], f64) and
+// k_backward_jac contracts them with it -- no second walk of the CT.
+template <typename VT, typename OT, int K>
+__global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
+    k_forward_jac(const VT* __restrict__ vol, const GridDev g,
+                  const double* __restrict__ frames, const DetDev det,
+                  OT* __restrict__ img, double* __restrict__ jac, size_t npix_total) {
+  extern __shared__ double tab[];
+  build_plane_table(g, tab);
+  __syncthreads();
+  int h, w, chunk;
+  tile_ray<K>(h, w, chunk);
+  const bool valid = h < det.H && w < det.W;
+  if (K == 1 && !valid) return;
+  const int b = blockIdx.z;
+  double part[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  double s[3], p[3], ah = 0.0, aw = 0.0;
+  Ray r;
+  r.hit = false;
+  if (valid) {
+    pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
+    ray_setup(g, s, p, r, K, chunk);
+    if (r.hit) {
+      BwdVisitor vis;
+      visitor_init(vis, tab + plane_table_len(g) + kWalkSmemDoublesPerThread * 128);
+      walk<VT, (K > 1)>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
+      double G[3], Hh[3];
+      visitor_sums(vis, G, Hh);
+      part[0] = vis.acc;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) { part[1 + a] = G[a]; part[4 + a] = Hh[a]; }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 7; ++k) part[k] = chunk_sum<K>(part[k]);
+  if (valid && chunk == 0) {
+    const size_t pix = (static_cast<size_t>(b) * det.H + h) * det.W + w;
+    const double L = ray_length(r);
+    double dEds[3] = {0.0, 0.0, 0.0}, dEdp[3] = {0.0, 0.0, 0.0};
+    if (part[0] != 0.0 || part[1] != 0.0 || part[2] != 0.0 || part[3] != 0.0 ||
+        part[4] != 0.0 || part[5] != 0.0 || part[6] != 0.0)
+      sums_to_endpoint_grads(r, part[0], part + 1, part + 4, L, dEds, dEdp);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      jac[a * npix_total + pix] = dEds[a];
+      jac[(3 + a) * npix_total + pix] = dEdp[a];
+    }
+    store_out(img + pix, L * part[0]);
+  }
+}
+
+// Contraction of the stored ray Jacobians with the upstream pixel gradient,
+// reduced per CTA in the same fixed order as k_backward (16 x 8 tiles, warp
+// butterflies, warps in index order), then k_reduce_frames.
+template <typename GT>
+__global__ void __launch_bounds__(kThreads)
+    k_backward_jac(const double* __restrict__ jac, size_t npix_total, const DetDev det,
+                   const GT* __restrict__ grad_img, double* __restrict__ partials) {
+  int h, w, chunk;
+  tile_ray<1>(h, w, chunk);
+  const int b = blockIdx.z;
+  double acc12[kFrameGrads];
+#pragma unroll
+  for (int k = 0; k < kFrameGrads; ++k) acc12[k] = 0.0;
+  if (h < det.H && w < det.W) {
+    const size_t pix = (static_cast<size_t>(b) * det.H + h) * det.W + w;
+    double js[3], jp[3];
+    bool any = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      js[a] = __ldg(jac + a * npix_total + pix);
+      jp[a] = __ldg(jac + (3 + a) * npix_total + pix);
+      any = any || js[a] != 0.0 || jp[a] != 0.0;
+    }
+    if (any) {  // a missed ray contributes exactly nothing (as in k_backward)
+      const double gpx = static_cast<double>(grad_img[pix]);
+      const double ah = (static_cast<double>(h) - det.half_h) * det.pitch_y;
+      const double aw = (static_cast<double>(w) - det.half_w) * det.pitch_x;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        acc12[a] = gpx * js[a];
+        acc12[3 + a] = gpx * jp[a];
+        acc12[6 + a] = gpx * ah * jp[a];
+        acc12[9 + a] = gpx * aw * jp[a];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kFrameGrads; ++k) {
+    double v = acc12[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    acc12[k] = v;
+  }
+  __shared__ double warp_part[kThreads / 32][kFrameGrads];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kFrameGrads; ++k) warp_part[warp][k] = acc12[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < kFrameGrads) {
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kThreads / 32; ++q) v += warp_part[q][threadIdx.x];
+    const int blocks_per_pose = gridDim.x * gridDim.y;
+    const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+    partials[(static_cast<size_t>(b) * blocks_per_pose + blk) * kFrameGrads +
+             threadIdx.x] = v;
+  }
+}
+
 // One CTA per pose: each thread sums a fixed strided subset of the CTA
 // partials, then a fixed shared-memory tree.
 constexpr int kReduceThreads = 128;
@@ -666,8 +784,85 @@ int drr_forward(const void* d_vol, int vol_dtype, const drr_grid* grid,
 size_t drr_backward_workspace_size(int32_t n_poses, const drr_detector* det) {
   drr::DetDev d;
   if (make_det(det, d) || n_poses < 0) return 0;
+  // max over the re-walk tiling (K threads per ray) and the Jacobian
+  // contraction's 16 x 8 tiles
   const dim3 grd = pose_grid(d, 1, ray_split(d, n_poses));
-  return static_cast<size_t>(n_poses) * grd.x * grd.y * drr::kFrameGrads * sizeof(double);
+  const dim3 grd1 = pose_grid(d, 1, 1);
+  const size_t tiles = grd.x * grd.y > grd1.x * grd1.y ? grd.x * grd.y : grd1.x * grd1.y;
+  return static_cast<size_t>(n_poses) * tiles * drr::kFrameGrads * sizeof(double);
+}
+
+int drr_forward_jac(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                    const double* d_frames, int32_t n_poses, const drr_detector* det,
+                    void* d_img, int img_dtype, double* d_jac, void* stream) {
+  drr::GridDev g;
+  drr::DetDev d;
+  int rc = make_grid(grid, g);
+  if (rc) return rc;
+  const size_t smem = table_bytes(g);
+  rc = make_det(det, d);
+  if (rc) return rc;
+  if (n_poses < 0 || n_poses > 65535)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
+  if (n_poses == 0) return DRR_OK;
+  if (d_jac == nullptr || d_img == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "d_img and d_jac must not be NULL");
+  if ((vol_dtype != DRR_VOL_F32 && vol_dtype != DRR_VOL_F64) || (img_dtype != 0 && img_dtype != 1))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "bad dtypes vol=%d img=%d", vol_dtype, img_dtype);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int K = ray_split(d, n_poses);
+  const dim3 grd = pose_grid(d, n_poses, K);
+  const size_t npix = static_cast<size_t>(n_poses) * d.H * d.W;
+  DRR_DISPATCH_K(K,
+    if (vol_dtype == DRR_VOL_F32 && img_dtype == 0) {
+      ensure_smem(drr::k_forward_jac<float, float, kK>, smem);
+      drr::k_forward_jac<float, float, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const float*>(d_vol), g, d_frames, d, static_cast<float*>(d_img), d_jac, npix);
+    } else if (vol_dtype == DRR_VOL_F32) {
+      ensure_smem(drr::k_forward_jac<float, double, kK>, smem);
+      drr::k_forward_jac<float, double, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const float*>(d_vol), g, d_frames, d, static_cast<double*>(d_img), d_jac, npix);
+    } else if (img_dtype == 1) {
+      ensure_smem(drr::k_forward_jac<double, double, kK>, smem);
+      drr::k_forward_jac<double, double, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const double*>(d_vol), g, d_frames, d, static_cast<double*>(d_img), d_jac, npix);
+    } else {
+      ensure_smem(drr::k_forward_jac<double, float, kK>, smem);
+      drr::k_forward_jac<double, float, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const double*>(d_vol), g, d_frames, d, static_cast<float*>(d_img), d_jac, npix);
+    })
+  return check_launch("drr_forward_jac");
+}
+
+int drr_backward_jac(const double* d_jac, int32_t n_poses, const drr_detector* det,
+                     const void* d_grad_img, int grad_dtype, double* d_grad_frames,
+                     void* d_workspace, size_t workspace_bytes, void* stream) {
+  drr::DetDev d;
+  int rc = make_det(det, d);
+  if (rc) return rc;
+  if (n_poses < 0 || n_poses > 65535)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
+  if (n_poses == 0) return DRR_OK;
+  const size_t need = drr_backward_workspace_size(n_poses, det);
+  if (workspace_bytes < need || d_workspace == nullptr)
+    return fail(DRR_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
+  if (grad_dtype != 0 && grad_dtype != 1)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "bad grad dtype %d", grad_dtype);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* partials = static_cast<double*>(d_workspace);
+  const dim3 grd = pose_grid(d, n_poses, 1);
+  const size_t npix = static_cast<size_t>(n_poses) * d.H * d.W;
+  if (grad_dtype == 0)
+    drr::k_backward_jac<float><<<grd, drr::kThreads, 0, st>>>(
+        d_jac, npix, d, static_cast<const float*>(d_grad_img), partials);
+  else
+    drr::k_backward_jac<double><<<grd, drr::kThreads, 0, st>>>(
+        d_jac, npix, d, static_cast<const double*>(d_grad_img), partials);
+  rc = check_launch("drr_backward_jac");
+  if (rc) return rc;
+  drr::k_reduce_frames<<<n_poses, drr::kReduceThreads, 0, st>>>(
+      partials, static_cast<int>(grd.x * grd.y), d_grad_frames);
+  return check_launch("drr_backward_jac/reduce");
 }
 
 int drr_backward(const void* d_vol, int vol_dtype, const drr_grid* grid,

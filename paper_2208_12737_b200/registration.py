@@ -4,9 +4,10 @@ Mirrors the reference's ``gradients.loss_and_gradient`` (``gradients.py:61-69``)
 and ``registration.register`` (``registration.py:89-125``), batched:
 
 * :func:`loss_and_gradient` -- B poses at once: ``drr_pose_frames`` ->
-  ``drr_forward`` -> ``drr_image_loss`` (fused neg-ZNCC / L2 value + pixel
-  gradient) -> ``drr_backward`` -> ``drr_pose_grad``.  Five native launches,
-  no host round trip, no torch autograd.
+  ``drr_forward_jac`` (image + per-ray Jacobian from one walk of each ray) ->
+  ``drr_image_loss`` (fused neg-ZNCC / L2 value + pixel gradient) ->
+  ``drr_backward_jac`` (walk-free contraction) -> ``drr_pose_grad``.  Native
+  launches only, no host round trip, no torch autograd.
 * :class:`RegistrationEngine` -- B independent momentum-GD registrations
   (``OptimizerConfig`` defaults = the paper's hyper-parameters,
   ``registration.py:41-58``).  Each iteration is the five launches above plus
@@ -97,6 +98,8 @@ class _Buffers:
         self.status = torch.zeros(B, dtype=torch.int32, device=dev)
         self.grad_frames = torch.empty((B, 12), dtype=torch.float64, device=dev)
         self.grad_eta = torch.empty((B, 7), dtype=torch.float64, device=dev)
+        # per-ray Jacobian of the one-walk forward (6 float64 per pixel)
+        self.jac = torch.empty((6, B * det.height * det.width), dtype=torch.float64, device=dev)
         lib = _lib.load()
         self.ws_bytes = lib.drr_backward_workspace_size(B, det.c)
         self.ws = torch.empty(max(self.ws_bytes, 8), dtype=torch.uint8, device=dev)
@@ -105,15 +108,15 @@ class _Buffers:
 def _launch_loss_grad(lib, vol, det, iso, eta, fixed, fixed_stride, kind, buf, stream):
     B = buf.B
     _lib.check(lib.drr_pose_frames(eta.data_ptr(), B, iso, buf.frames.data_ptr(), stream))
-    _lib.check(lib.drr_forward(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
-                               buf.frames.data_ptr(), B, det.c, buf.img.data_ptr(), 0, stream))
+    _lib.check(lib.drr_forward_jac(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
+                                   buf.frames.data_ptr(), B, det.c, buf.img.data_ptr(), 0,
+                                   buf.jac.data_ptr(), stream))
     _lib.check(lib.drr_image_loss(buf.img.data_ptr(), fixed.data_ptr(), 0, fixed_stride, B,
                                   det.height * det.width, kind, buf.value.data_ptr(),
                                   buf.pix_grad.data_ptr(), buf.status.data_ptr(), stream))
-    _lib.check(lib.drr_backward(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
-                                buf.frames.data_ptr(), B, det.c, buf.pix_grad.data_ptr(), 0,
-                                buf.grad_frames.data_ptr(), None, 0, buf.ws.data_ptr(),
-                                buf.ws_bytes, stream))
+    _lib.check(lib.drr_backward_jac(buf.jac.data_ptr(), B, det.c, buf.pix_grad.data_ptr(), 0,
+                                    buf.grad_frames.data_ptr(), buf.ws.data_ptr(),
+                                    buf.ws_bytes, stream))
 
 
 def _prep_fixed(fixed, B, det, dev):

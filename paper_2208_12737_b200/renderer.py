@@ -14,9 +14,10 @@ equivalent of the reference's ``render`` / ``render_with_gradient`` /
   on the device as float32 in the reference's x-fastest flat layout
   (``volume.py:77-79``).
 
-The image comes from ``drr_forward`` and its gradient from ``drr_backward``
-(one fused re-walk that reduces dL/d(frame) on the device); torch autograd only
-chains the 12 frame numbers to the pose (``geometry.pose_frames``).
+With a gradient requested, the image and every ray's endpoint Jacobian come
+from one walk (``drr_forward_jac``) and backward is a walk-free contraction
+(``drr_backward_jac``); without one, ``drr_forward`` alone runs.  torch autograd
+only chains the 12 frame numbers to the pose (``geometry.pose_frames``).
 """
 
 from __future__ import annotations
@@ -143,6 +144,45 @@ def backward_frames(vol: DeviceVolume, det: Detector, frames: torch.Tensor,
     return (grad_frames, img) if want_image else grad_frames
 
 
+def jac_bytes(det: Detector, n_poses: int) -> int:
+    """Bytes of the stored ray Jacobian for n_poses (6 float64 per pixel)."""
+    return 6 * 8 * int(n_poses) * det.height * det.width
+
+
+def render_frames_jac(vol: DeviceVolume, det: Detector, frames: torch.Tensor,
+                      out_dtype=torch.float32):
+    """Image (B, H, W) plus the per-ray Jacobian (6, B*H*W) float64 from ONE
+    walk (``drr_forward_jac``); :func:`backward_from_jac` turns it into dL/dframe."""
+    _require_cuda(frames, "frames")
+    frames = frames.detach().to(torch.float64).contiguous()
+    B = frames.shape[0]
+    img = torch.empty((B, det.height, det.width), dtype=out_dtype, device=frames.device)
+    jac = torch.empty((6, B * det.height * det.width), dtype=torch.float64, device=frames.device)
+    lib = _lib.load()
+    _lib.check(lib.drr_forward_jac(vol.flat.data_ptr(), vol.vol_dtype, vol.grid, frames.data_ptr(),
+                                   B, det.c, img.data_ptr(),
+                                   1 if out_dtype == torch.float64 else 0, jac.data_ptr(),
+                                   _stream_ptr(frames.device)))
+    return img, jac
+
+
+def backward_from_jac(det: Detector, jac: torch.Tensor, grad_img: torch.Tensor) -> torch.Tensor:
+    """dL/d(frame) (B, 12) from a stored ray Jacobian (``drr_backward_jac``, no walk)."""
+    if grad_img.dtype not in (torch.float32, torch.float64):
+        grad_img = grad_img.to(torch.float32)
+    grad_img = grad_img.contiguous()
+    B = grad_img.shape[0]
+    lib = _lib.load()
+    ws_bytes = lib.drr_backward_workspace_size(B, det.c)
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=grad_img.device)
+    grad_frames = torch.empty((B, 12), dtype=torch.float64, device=grad_img.device)
+    _lib.check(lib.drr_backward_jac(jac.data_ptr(), B, det.c, grad_img.data_ptr(),
+                                    1 if grad_img.dtype == torch.float64 else 0,
+                                    grad_frames.data_ptr(), ws.data_ptr(), ws_bytes,
+                                    _stream_ptr(grad_img.device)))
+    return grad_frames
+
+
 def count_steps(vol: DeviceVolume, det: Detector, frames: torch.Tensor) -> torch.Tensor:
     """Used voxel-steps per ray (B, H, W) int32 (python_ref.ray_structure's `use`)."""
     frames = frames.detach().to(torch.float64).contiguous()
@@ -155,19 +195,37 @@ def count_steps(vol: DeviceVolume, det: Detector, frames: torch.Tensor) -> torch
     return steps
 
 
+# Above this many bytes of stored ray Jacobian, autograd re-walks the rays in
+# backward instead (drr_backward) -- e.g. 64 poses at 1024^2 would hold 3.2 GB.
+JAC_BUDGET_BYTES = 2 << 30
+
+
 class _RenderFrames(torch.autograd.Function):
-    """frames (B, 12) -> image (B, H, W); backward = the fused CUDA re-walk."""
+    """frames (B, 12) -> image (B, H, W).
+
+    When a gradient is needed, forward is ``drr_forward_jac`` (one walk: image
+    plus per-ray Jacobian) and backward the walk-free ``drr_backward_jac``;
+    above ``JAC_BUDGET_BYTES`` forward is ``drr_forward`` and backward the
+    fused re-walk ``drr_backward``."""
 
     @staticmethod
     def forward(ctx, frames, vol, det):
-        ctx.save_for_backward(frames)
         ctx.vol, ctx.det = vol, det
+        if ctx.needs_input_grad[0] and jac_bytes(det, frames.shape[0]) <= JAC_BUDGET_BYTES:
+            img, jac = render_frames_jac(vol, det, frames)
+            ctx.save_for_backward(frames, jac)
+            return img
+        ctx.save_for_backward(frames)
         return render_frames(vol, det, frames)
 
     @staticmethod
     def backward(ctx, grad_img):
-        (frames,) = ctx.saved_tensors
-        grad_frames = backward_frames(ctx.vol, ctx.det, frames, grad_img)
+        saved = ctx.saved_tensors
+        frames = saved[0]
+        if len(saved) == 2:
+            grad_frames = backward_from_jac(ctx.det, saved[1], grad_img)
+        else:
+            grad_frames = backward_frames(ctx.vol, ctx.det, frames, grad_img)
         return grad_frames.to(frames.dtype), None, None
 
 

@@ -10,7 +10,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2208_12737_b200 import DRR, backward_frames, count_steps, pose_frames, render_frames, synthetic
+from paper_2208_12737_b200 import (DRR, backward_frames, backward_from_jac, count_steps, pose_frames,
+                                   render_frames, render_frames_jac, synthetic)
 
 dev = torch.device("cuda")
 vol = synthetic.chest_phantom()
@@ -23,18 +24,23 @@ for B in [int(x) for x in (sys.argv[1:] or ["32", "1"])]:
     frames = pose_frames(torch.tensor(poses, device=dev), drr.isocenter)
     S = float(count_steps(drr.volume, drr.detector, frames).double().sum())
     g = torch.randn((B, 200, 200), device=dev)
-    tf, tb = [], []
+    fns = {"fwd": lambda: render_frames(drr.volume, drr.detector, frames),
+           "bwd": lambda: backward_frames(drr.volume, drr.detector, frames, g),
+           "fj": lambda: hold.__setitem__(0, render_frames_jac(drr.volume, drr.detector, frames)[1]),
+           "bj": lambda: backward_from_jac(drr.detector, hold[0], g)}
+    hold = {}
+    t = {k: [] for k in fns}
     for i in range(12):
-        flush.fill_(1)
-        a, b = torch.cuda.Event(True), torch.cuda.Event(True)
-        a.record(); render_frames(drr.volume, drr.detector, frames); b.record(); b.synchronize()
-        flush.fill_(1)
-        c, d = torch.cuda.Event(True), torch.cuda.Event(True)
-        c.record(); backward_frames(drr.volume, drr.detector, frames, g); d.record(); d.synchronize()
-        if i >= 2:
-            tf.append(a.elapsed_time(b)); tb.append(c.elapsed_time(d))
-    f, bw = float(np.median(tf)), float(np.median(tb))
-    res[B] = {"fwd_ms": f, "bwd_ms": bw, "steps_per_drr": S / B,
-              "fwd_gsteps_s": S / f / 1e6, "bwd_gsteps_s": S / bw / 1e6,
-              "fwd_bwd_drr_s": B / ((f + bw) / 1e3)}
+        for k, fn in fns.items():
+            flush.fill_(1)
+            a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+            a.record(); fn(); b.record(); b.synchronize()
+            if i >= 2:
+                t[k].append(a.elapsed_time(b))
+    m = {k: float(np.median(v)) for k, v in t.items()}
+    res[B] = {"fwd_ms": m["fwd"], "bwd_ms": m["bwd"], "fwd_jac_ms": m["fj"], "bwd_jac_ms": m["bj"],
+              "steps_per_drr": S / B,
+              "fwd_gsteps_s": S / m["fwd"] / 1e6, "fwd_jac_gsteps_s": S / m["fj"] / 1e6,
+              "rewalk_drr_s": B / ((m["fwd"] + m["bwd"]) / 1e3),
+              "one_walk_drr_s": B / ((m["fj"] + m["bj"]) / 1e3)}
 print(json.dumps(res))

@@ -69,6 +69,7 @@ def test_invalid_arguments_map_to_reference_errors():
 
 def test_workspace_size_and_error():
     from paper_2208_12737_b200 import _lib
+    from paper_2208_12737_b200.errors import InvalidArgumentError
     lib = _lib.load()
     det = _lib.make_detector(200, 200, 3.6, 3.6, ray_split=1)
     # one thread per ray: 13 x 25 CTA tiles of 16 x 8 pixels, 12 doubles each, per pose
@@ -87,6 +88,13 @@ def test_workspace_size_and_error():
     assert rc == _lib.DRR_ERR_WORKSPACE
     with pytest.raises(Exception, match="workspace"):
         _lib.check(rc)
+    # the Jacobian contraction validates its workspace the same way
+    rc = lib.drr_backward_jac(None, 3, det, None, 0, None, None, 16, None)
+    assert rc == _lib.DRR_ERR_WORKSPACE
+    assert lib.drr_backward_jac(None, 0, det, None, 0, None, None, 0, None) == _lib.DRR_OK
+    with pytest.raises(InvalidArgumentError, match="NULL"):
+        _lib.check(lib.drr_forward_jac(None, 0, grid, None, 1, det, None, 0, None, None))
+    assert lib.drr_forward_jac(None, 0, grid, None, 0, det, None, 0, None, None) == _lib.DRR_OK
 
 
 def test_volume_size_limit():

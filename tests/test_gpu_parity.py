@@ -346,3 +346,78 @@ def test_ray_split_matches_single_thread(split, cuda_device):
         ga = backward_frames(vol, d1, f, g).cpu().numpy()
         gb = backward_frames(vol, dk, f, g).cpu().numpy()
         np.testing.assert_allclose(gb, ga, rtol=0, atol=1e-11 * np.abs(ga).max())
+
+
+@pytest.mark.parametrize("split", [1, 2, 8])
+def test_forward_jac_matches_forward_and_rewalk(split, golden, cuda_device):
+    """drr_forward_jac + drr_backward_jac (one CT walk per ray, gradient by
+    contracting the stored ray Jacobians) against drr_forward (image: bitwise)
+    and the fused re-walk drr_backward (frame gradients: bitwise at K = 1, the
+    same fixed reduction order), and against the oracle's reverse-mode render
+    backward on the C2 chest and the golden sphere poses."""
+    from paper_2208_12737_b200 import (DeviceVolume, Detector, backward_frames,
+                                       backward_from_jac, render_frames, render_frames_jac,
+                                       synthetic)
+    rng = np.random.default_rng(7)
+    vol = _vol_from_golden(golden, "ps_")
+    det = Detector(21, 21, 4.0, ray_split=split)
+    frames = torch.tensor(np.stack([O.pose_frame(e, golden["ps_center"]) for e in golden["ps_poses"]]),
+                          device=cuda_device)
+    g_img = rng.normal(size=(frames.shape[0], 21, 21))
+    img, jac = render_frames_jac(vol, det, frames, out_dtype=torch.float64)
+    assert torch.equal(img, render_frames(vol, det, frames, out_dtype=torch.float64))
+    gt = torch.tensor(g_img, device=cuda_device)
+    got = backward_from_jac(det, jac, gt).cpu().numpy()
+    again = backward_from_jac(det, jac, gt).cpu().numpy()
+    np.testing.assert_array_equal(got, again)
+    rewalk = backward_frames(vol, det, frames, gt).cpu().numpy()
+    if split == 1:
+        np.testing.assert_array_equal(got, rewalk)
+    for b, eta in enumerate(golden["ps_poses"]):
+        frame = O.pose_frame(eta, golden["ps_center"])
+        _, ref = O.render_backward(golden["ps_flat"], golden["ps_dims"], golden["ps_spacing"],
+                                   golden["ps_origin"], frame, 21, 21, 4.0, 4.0, g_img[b])
+        np.testing.assert_allclose(got[b], ref, atol=1e-10 * np.abs(ref).max(), rtol=0)
+    # C2 chest, fp32 product layout, oblique pose
+    chest = synthetic.chest_phantom()
+    spacing = (0.703125, 0.703125, 2.5)
+    cv = DeviceVolume(chest, spacing)
+    cdet = Detector(200, 200, 3.6, ray_split=split)
+    eta = np.array([300.0, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0])
+    frame = O.pose_frame(eta, cv.center)
+    ft = torch.tensor(frame, device=cuda_device)[None]
+    img, jac = render_frames_jac(cv, cdet, ft, out_dtype=torch.float64)
+    flat = chest.astype(np.float64).ravel(order="F")
+    ref_img = O.render(flat, chest.shape, spacing, (0, 0, 0), frame, 200, 200, 3.6, 3.6)
+    if split == 1:
+        np.testing.assert_array_equal(img[0].cpu().numpy(), ref_img)
+    else:
+        np.testing.assert_allclose(img[0].cpu().numpy(), ref_img, rtol=1e-13, atol=1e-12)
+    g2 = rng.normal(size=(200, 200))
+    got = backward_from_jac(cdet, jac, torch.tensor(g2, device=cuda_device)[None]).cpu().numpy()[0]
+    _, refg = O.render_backward(flat, chest.shape, spacing, (0, 0, 0), frame, 200, 200, 3.6, 3.6, g2)
+    np.testing.assert_allclose(got, refg, atol=1e-9 * np.abs(refg).max(), rtol=0)
+
+
+def test_module_uses_one_walk_and_rewalk_fallback(golden, cuda_device, monkeypatch):
+    """The nn.Module's autograd path: with a gradient requested it runs the
+    one-walk forward + Jacobian contraction; above the Jacobian memory budget
+    it re-walks in backward.  Both give the same pose gradient."""
+    from paper_2208_12737_b200 import DRR, renderer
+    from paper_2208_12737_b200.metrics import neg_zncc
+    dims = tuple(int(n) for n in golden["ps_dims"])
+    data = golden["ps_flat"].reshape(dims[::-1]).transpose(2, 1, 0)
+    fixed = torch.tensor(golden["ps_fixed"], device=cuda_device)
+    eta = golden["ps_poses"][1]
+    drr = DRR(data, 2.0, sdr=float(eta[0]), height=21, delx=4.0, device=cuda_device)
+
+    def grad():
+        rot = torch.tensor(eta[1:4], device=cuda_device, requires_grad=True)
+        tra = torch.tensor(eta[4:7], device=cuda_device, requires_grad=True)
+        neg_zncc(drr(rot, tra), fixed).backward()
+        return torch.cat([rot.grad, tra.grad]).cpu().numpy()
+
+    one_walk = grad()
+    monkeypatch.setattr(renderer, "JAC_BUDGET_BYTES", 0)
+    rewalk = grad()
+    np.testing.assert_allclose(one_walk, rewalk, rtol=1e-12, atol=1e-15)
