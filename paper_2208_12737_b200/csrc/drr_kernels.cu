@@ -23,6 +23,7 @@
 
 #include "../../include/drr_b200.h"
 #include "siddon_walk.cuh"
+#include "siddon_lean.cuh"
 #include "loss_kernels.cuh"
 #include "pose_kernels.cuh"
 
@@ -38,17 +39,15 @@ namespace drr {
 #else
 #define DRR_LB __launch_bounds__(kThreads)
 #endif
-// The backward re-walk carries 13 more live doubles than the forward; capping
-// it at <= 96 registers (5 CTAs/SM) measured faster than ptxas's 111
-// (profiles/r01_v2 A/B: 4.34 vs 4.93 ms for 32 C2 poses).
+// Launch bounds (A/B on C2, 32 poses, walk v5 with a 3-deep gather pipeline):
+// the gradient walks (k_forward_jac, k_backward) at 4 CTAs/SM (<= 128
+// registers, no spills) and the forward at 6 CTAs/SM (<= 80) beat 5 and 8
+// CTAs/SM, where ptxas spilled: 3.08 vs 3.74 ms and 2.19 vs 2.56 ms.
 #ifndef DRR_BWD_MINB
-#define DRR_BWD_MINB 5
+#define DRR_BWD_MINB 4
 #endif
-// Forward, one thread per ray: 8 CTAs/SM (<= 64 registers; ptxas alone picks
-// 72 = 7 CTAs): 2.84 vs 3.01 ms for 32 C2 poses.  Split rays (K > 1, few
-// rays) measured faster without the bound.
 #ifndef DRR_FWD_MINB
-#define DRR_FWD_MINB 8
+#define DRR_FWD_MINB 6
 #endif
 #ifndef DRR_SPLIT_MINB
 #define DRR_SPLIT_MINB 6
@@ -123,67 +122,6 @@ __device__ __forceinline__ void store_out(OT* p, double v) {
   *p = static_cast<OT>(v);
 }
 
-// ---------------------------------------------------------------- forward
-template <typename VT, typename OT, int K>
-__global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FWD_MINB : DRR_SPLIT_MINB)
-    k_forward(const VT* __restrict__ vol, const GridDev g,
-              const double* __restrict__ frames, const DetDev det,
-              OT* __restrict__ img) {
-  extern __shared__ double tab[];
-  build_plane_table(g, tab);
-  __syncthreads();
-  int h, w, chunk;
-  tile_ray<K>(h, w, chunk);
-  const bool valid = h < det.H && w < det.W;
-  if (K == 1 && !valid) return;
-  const int b = blockIdx.z;
-  double acc = 0.0, L = 0.0;
-  if (valid) {
-    double s[3], p[3], ah, aw;
-    pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
-    Ray r;
-    ray_setup(g, s, p, r, K, chunk);
-    L = ray_length(r);
-    if (r.hit) {
-      SumVisitor vis;
-      walk<VT, (K > 1)>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
-      acc = vis.acc;
-    }
-  }
-  acc = chunk_sum<K>(acc);
-  if (valid && chunk == 0)
-    store_out(img + (static_cast<size_t>(b) * det.H + h) * det.W + w, L * acc);
-}
-
-template <typename VT, int K>
-__global__ void DRR_LB
-    k_count(const VT* __restrict__ vol, const GridDev g,
-            const double* __restrict__ frames, const DetDev det,
-            int* __restrict__ steps) {
-  extern __shared__ double tab[];
-  build_plane_table(g, tab);
-  __syncthreads();
-  int h, w, chunk;
-  tile_ray<K>(h, w, chunk);
-  const bool valid = h < det.H && w < det.W;
-  if (K == 1 && !valid) return;
-  const int b = blockIdx.z;
-  int n = 0;
-  if (valid) {
-    double s[3], p[3], ah, aw;
-    pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
-    Ray r;
-    ray_setup(g, s, p, r, K, chunk);
-    if (r.hit) {
-      CountVisitor vis;
-      walk<VT, (K > 1)>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
-      n = vis.steps;
-    }
-  }
-  n = chunk_sum<K>(n);
-  if (valid && chunk == 0) steps[(static_cast<size_t>(b) * det.H + h) * det.W + w] = n;
-}
-
 // Endpoint gradients of one ray from the reverse-mode visitor
 // (see orc_raysum_endpoint_grad in oracle/siddon_oracle.c for the algebra).
 __device__ __forceinline__ void visitor_sums(const GradVisitor& v, double* G, double* Hh) {
@@ -203,6 +141,100 @@ using BwdVisitor = GradVisitor;
 
 __device__ __forceinline__ void visitor_init(GradVisitor&, double*) {}
 __device__ __forceinline__ void visitor_init(GradVisitorSmem& v, double* slots) { v.init(slots); }
+
+// Walk v5 (siddon_lean.cuh) by default; DRR_LEAN=0 builds the v4 visitor walk
+// for A/B.
+#ifndef DRR_LEAN
+#define DRR_LEAN 1
+#endif
+
+template <typename VT, int kMode, bool kChunked>
+__device__ __forceinline__ void walk_sums(const VT* __restrict__ vol, const GridDev& g,
+                                          double* tab, const Ray& r, LeanSums& o) {
+#if DRR_LEAN
+  lean_walk<VT, kMode>(vol, g, tab, tab + plane_table_span(g), r, o);
+#else
+  if (kMode == kLeanSum) {
+    SumVisitor v;
+    walk<VT, kChunked>(vol, g, tab, tab + plane_table_span(g), r, v);
+    o.acc = v.acc;
+  } else if (kMode == kLeanCount) {
+    CountVisitor v;
+    walk<VT, kChunked>(vol, g, tab, tab + plane_table_span(g), r, v);
+    o.steps = v.steps;
+  } else {
+    BwdVisitor v;
+    visitor_init(v, tab + plane_table_span(g) + kWalkSmemDoublesPerThread * 128);
+    walk<VT, kChunked>(vol, g, tab, tab + plane_table_span(g), r, v);
+    double G[3], Hh[3];
+    visitor_sums(v, G, Hh);
+    o.acc = v.acc;
+    o.G0 = G[0]; o.G1 = G[1]; o.G2 = G[2];
+    o.H0 = Hh[0]; o.H1 = Hh[1]; o.H2 = Hh[2];
+  }
+#endif
+}
+
+// ---------------------------------------------------------------- forward
+template <typename VT, typename OT, int K>
+__global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FWD_MINB : DRR_SPLIT_MINB)
+    k_forward(const VT* __restrict__ vol, const GridDev g,
+              const double* __restrict__ frames, const DetDev det,
+              OT* __restrict__ img) {
+  extern __shared__ __align__(16) double tab[];
+  build_plane_table(g, tab);
+  __syncthreads();
+  int h, w, chunk;
+  tile_ray<K>(h, w, chunk);
+  const bool valid = h < det.H && w < det.W;
+  if (K == 1 && !valid) return;
+  const int b = blockIdx.z;
+  double acc = 0.0, L = 0.0;
+  if (valid) {
+    double s[3], p[3], ah, aw;
+    pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
+    Ray r;
+    ray_setup(g, s, p, r, K, chunk);
+    L = ray_length(r);
+    if (r.hit) {
+      LeanSums o;
+      walk_sums<VT, kLeanSum, (K > 1)>(vol, g, tab, r, o);
+      acc = o.acc;
+    }
+  }
+  acc = chunk_sum<K>(acc);
+  if (valid && chunk == 0)
+    store_out(img + (static_cast<size_t>(b) * det.H + h) * det.W + w, L * acc);
+}
+
+template <typename VT, int K>
+__global__ void DRR_LB
+    k_count(const VT* __restrict__ vol, const GridDev g,
+            const double* __restrict__ frames, const DetDev det,
+            int* __restrict__ steps) {
+  extern __shared__ __align__(16) double tab[];
+  build_plane_table(g, tab);
+  __syncthreads();
+  int h, w, chunk;
+  tile_ray<K>(h, w, chunk);
+  const bool valid = h < det.H && w < det.W;
+  if (K == 1 && !valid) return;
+  const int b = blockIdx.z;
+  int n = 0;
+  if (valid) {
+    double s[3], p[3], ah, aw;
+    pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
+    Ray r;
+    ray_setup(g, s, p, r, K, chunk);
+    if (r.hit) {
+      LeanSums o;
+      walk_sums<VT, kLeanCount, (K > 1)>(vol, g, tab, r, o);
+      n = o.steps;
+    }
+  }
+  n = chunk_sum<K>(n);
+  if (valid && chunk == 0) steps[(static_cast<size_t>(b) * det.H + h) * det.W + w] = n;
+}
 
 template <typename V>
 __device__ __forceinline__ void endpoint_grads(const Ray& r,
@@ -248,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
                const double* __restrict__ frames, const DetDev det,
                const GT* __restrict__ grad_img, OT* __restrict__ img,
                double* __restrict__ partials) {
-  extern __shared__ double tab[];
+  extern __shared__ __align__(16) double tab[];
   build_plane_table(g, tab);
   __syncthreads();
   int h, w, chunk;
@@ -267,14 +299,11 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
     pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
     ray_setup(g, s, p, r, K, chunk);
     if (r.hit) {
-      BwdVisitor vis;
-      visitor_init(vis, tab + plane_table_len(g) + kWalkSmemDoublesPerThread * 128);
-      walk<VT, (K > 1)>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
-      double G[3], Hh[3];
-      visitor_sums(vis, G, Hh);
-      part[0] = vis.acc;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) { part[1 + a] = G[a]; part[4 + a] = Hh[a]; }
+      LeanSums o;
+      walk_sums<VT, kLeanGrad, (K > 1)>(vol, g, tab, r, o);
+      part[0] = o.acc;
+      part[1] = o.G0; part[2] = o.G1; part[3] = o.G2;
+      part[4] = o.H0; part[5] = o.H1; part[6] = o.H2;
     }
   }
 #pragma unroll
@@ -339,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
     k_forward_jac(const VT* __restrict__ vol, const GridDev g,
                   const double* __restrict__ frames, const DetDev det,
                   OT* __restrict__ img, double* __restrict__ jac, size_t npix_total) {
-  extern __shared__ double tab[];
+  extern __shared__ __align__(16) double tab[];
   build_plane_table(g, tab);
   __syncthreads();
   int h, w, chunk;
@@ -355,14 +384,11 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
     pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
     ray_setup(g, s, p, r, K, chunk);
     if (r.hit) {
-      BwdVisitor vis;
-      visitor_init(vis, tab + plane_table_len(g) + kWalkSmemDoublesPerThread * 128);
-      walk<VT, (K > 1)>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
-      double G[3], Hh[3];
-      visitor_sums(vis, G, Hh);
-      part[0] = vis.acc;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) { part[1 + a] = G[a]; part[4 + a] = Hh[a]; }
+      LeanSums o;
+      walk_sums<VT, kLeanGrad, (K > 1)>(vol, g, tab, r, o);
+      part[0] = o.acc;
+      part[1] = o.G0; part[2] = o.G1; part[3] = o.G2;
+      part[4] = o.H0; part[5] = o.H1; part[6] = o.H2;
     }
   }
 #pragma unroll
@@ -483,7 +509,7 @@ __global__ void __launch_bounds__(kRayThreads)
     k_raysum(const VT* __restrict__ vol, const GridDev g,
              const double* __restrict__ src, const double* __restrict__ pix,
              int64_t n_rays, double* __restrict__ out) {
-  extern __shared__ double tab[];
+  extern __shared__ __align__(16) double tab[];
   build_plane_table(g, tab);
   __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -494,9 +520,9 @@ __global__ void __launch_bounds__(kRayThreads)
   ray_setup(g, s, p, r);
   double e = 0.0;
   if (r.hit) {
-    SumVisitor vis;
-    walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
-    e = ray_length(r) * vis.acc;
+    LeanSums o;
+    walk_sums<VT, kLeanSum, false>(vol, g, tab, r, o);
+    e = ray_length(r) * o.acc;
   }
   out[i] = e;
 }
@@ -508,7 +534,7 @@ __global__ void __launch_bounds__(kRayThreads)
                   const double* __restrict__ pix, int64_t n_rays,
                   double* __restrict__ out, double* __restrict__ dEds,
                   double* __restrict__ dEdp) {
-  extern __shared__ double tab[];
+  extern __shared__ __align__(16) double tab[];
   build_plane_table(g, tab);
   __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -519,12 +545,12 @@ __global__ void __launch_bounds__(kRayThreads)
   ray_setup(g, s, p, r);
   double e = 0.0, gs[3] = {0.0, 0.0, 0.0}, gp[3] = {0.0, 0.0, 0.0};
   if (r.hit) {
-    BwdVisitor vis;
-    visitor_init(vis, tab + plane_table_len(g) + kWalkSmemDoublesPerThread * 128);
-    walk<VT>(vol, g, tab, tab + drr::plane_table_len(g), r, vis);
+    LeanSums o;
+    walk_sums<VT, kLeanGrad, false>(vol, g, tab, r, o);
     const double L = ray_length(r);
-    e = L * vis.acc;
-    endpoint_grads(r, vis, L, gs, gp);
+    e = L * o.acc;
+    const double G[3] = {o.G0, o.G1, o.G2}, Hh[3] = {o.H0, o.H1, o.H2};
+    sums_to_endpoint_grads(r, o.acc, G, Hh, L, gs, gp);
   }
   out[i] = e;
 #pragma unroll
@@ -559,9 +585,12 @@ int check_launch(const char* what) {
 // Dynamic shared memory for the per-CTA plane table; >48 KB needs opt-in.
 size_t table_bytes(const drr::GridDev& g) {
   // plane table + the walk's per-thread constants (both kernels use <= 128 threads)
-  return (static_cast<size_t>(drr::plane_table_len(g)) +
-          static_cast<size_t>(drr::kWalkSmemDoublesPerThread + drr::kGradSmemDoublesPerThread) *
-              128) * sizeof(double);
+#if DRR_LEAN
+  const size_t per_thread = drr::kLeanRecDoublesPerThread;
+#else
+  const size_t per_thread = drr::kWalkSmemDoublesPerThread + drr::kGradSmemDoublesPerThread;
+#endif
+  return (static_cast<size_t>(drr::plane_table_span(g)) + per_thread * 128) * sizeof(double);
 }
 
 template <typename Kernel>

@@ -1,0 +1,279 @@
+// siddon_lean.cuh -- the counted, select-light Siddon walk (walk v5).
+//
+// Same segments, same arithmetic, same order as walk_select in
+// siddon_walk.cuh (and therefore as the reference, _native.pyx:140-193);
+// what changes is the instruction budget per voxel-step, which is what bounds
+// the kernel (ncu r01: issue-bound, ALU and FP64 pipes busiest, DRAM below
+// the algorithmic bytes):
+//  * the number of crossings of the ray (or chunk) is counted at setup
+//    (Ray::count, exact with the reference's [amin, amax] filter and the
+//    chunk tie rule), so the loop has no end-of-ray compare/select;
+//  * the winning axis is carried as one-hot 0/1 integers: the per-axis state
+//    updates are integer multiply-adds (FMA pipe) instead of ALU selects, and
+//    the reverse-mode sums (G_a, H_a) are FMAs by 0.0/1.0 masks;
+//  * the winner's ray constants (s, d, 1/d) come from a per-thread record in
+//    shared memory indexed by the axis (one LDS.128 + one LDS.64) instead of a
+//    twelve-instruction select tree; the exact-voxel path reads s, d there too,
+//    so the Ray itself is dead inside the loop;
+//  * each axis keeps the shared-memory byte address of its next-next plane;
+//  * seg > max(T, 1e-12) is the single fast-path test (used and certified
+//    voxel); everything else takes the reference's exact path out of line;
+//  * the gather is a predicated load into a zeroed register, consumed one
+//    iteration later, so no instruction waits on it in the issuing iteration.
+#pragma once
+#include "siddon_walk.cuh"
+
+namespace drr {
+
+// Per-thread shared-memory record: {s_a, d_a} (16 B) and 1/d_a (8 B) per
+// axis, structure-of-arrays over the CTA's threads (conflict-free LDS.128).
+constexpr int kLeanRecDoublesPerThread = 9;
+constexpr int kLeanThreads = 128;  // threads per CTA of every kernel using the walk
+// Gather pipeline depth: a segment's voxel value is consumed kLeanPipe steps
+// after its load is issued (ncu lean1: 45% of stall samples waited on the
+// gather when it was consumed one step later).
+#ifndef DRR_LEAN_PIPE
+#define DRR_LEAN_PIPE 3
+#endif
+constexpr int kLeanPipe = DRR_LEAN_PIPE;
+
+enum LeanMode { kLeanSum = 0, kLeanCount = 1, kLeanGrad = 2 };
+
+struct LeanSums {
+  double acc = 0.0;
+  double G0 = 0.0, G1 = 0.0, G2 = 0.0, H0 = 0.0, H1 = 0.0, H2 = 0.0;
+  int steps = 0;
+};
+
+// One-hot axis masks of a crossing label (label 3 = clip: all zero, no
+// tangent), as 0/1 integers.
+struct LabMask {
+  int m0, m1, m2;
+};
+__device__ __forceinline__ LabMask lab_mask(int lab) {
+  return LabMask{lab == 0, lab == 1, lab == 2};
+}
+// 0.0 / 1.0 from a 0/1 mask (high word only, on the integer FMA pipe)
+__device__ __forceinline__ double mask_d(int m) { return __hiloint2double(m * 0x3FF00000, 0); }
+
+// G_lab += c and H_lab += c * alpha as masked FMAs: no per-lane branch and no
+// select tree (c * 1 and c * 0 are exact; H rounds c * alpha once before the
+// add, ~1 ulp of one term -- the oracle comparison bar is 1e-10 relative).
+__device__ __forceinline__ void lean_apply(LeanSums& o, const LabMask& m, double a, double c) {
+  const double ca = c * a;
+  const double k0 = mask_d(m.m0), k1 = mask_d(m.m1), k2 = mask_d(m.m2);
+  o.G0 = __fma_rn(c, k0, o.G0);
+  o.G1 = __fma_rn(c, k1, o.G1);
+  o.G2 = __fma_rn(c, k2, o.G2);
+  o.H0 = __fma_rn(ca, k0, o.H0);
+  o.H1 = __fma_rn(ca, k1, o.H1);
+  o.H2 = __fma_rn(ca, k2, o.H2);
+}
+
+// A segment whose gather is in flight: length, value (0 if unused), the
+// used flag, and the label mask and parameter of its starting crossing.
+template <typename VT>
+struct LeanStage {
+  double seg = 0.0, a = 0.0;
+  VT v = VT(0);
+  int used = 0;
+  LabMask m{0, 0, 0};
+};
+
+template <int kMode, typename VT>
+__device__ __forceinline__ void lean_consume(LeanSums& o, double& pend, double seg, VT v,
+                                             int used, const LabMask& m, double a) {
+  if (kMode == kLeanCount) {
+    o.steps += used;
+    return;
+  }
+  const double vv = static_cast<double>(v);  // 0 for unused segments
+  o.acc = o.acc + seg * vv;                    // _native.pyx:187 (TU is --fmad=false)
+  if (kMode == kLeanGrad) {
+    lean_apply(o, m, a, pend - vv);
+    pend = vv;
+  }
+}
+
+template <int kMode>
+__device__ __forceinline__ void lean_finish(LeanSums& o, double pend, int lab, double a) {
+  if (kMode == kLeanGrad) lean_apply(o, lab_mask(lab), a, pend);
+}
+
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void lds_2f64(uint32_t addr, double& a, double& b) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr));
+}
+
+// Predicated gather: v = used ? vol[idx] : 0, with no branch around the load
+// (so nothing in this iteration depends on its arrival).
+__device__ __forceinline__ float gather(const float* __restrict__ vol, int idx, int used) {
+  float v;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %2, 0;\n\tmov.b32 %0, 0;\n\t"
+               "@p ld.global.nc.f32 %0, [%1];\n\t}"
+               : "=f"(v) : "l"(vol + idx), "r"(used));
+  return v;
+}
+__device__ __forceinline__ double gather(const double* __restrict__ vol, int idx, int used) {
+  double v;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %2, 0;\n\tmov.b64 %0, 0;\n\t"
+               "@p ld.global.nc.f64 %0, [%1];\n\t}"
+               : "=d"(v) : "l"(vol + idx), "r"(used));
+  return v;
+}
+
+// Exact path (out of the fast path): the used test and the reference's
+// floored midpoint (_native.pyx:68-82, 186), with s and d from the record.
+// Returns the voxel, or -1 for a skipped segment.
+__device__ __forceinline__ int lean_exact(const GridDev& g, uint32_t sd_s, uint32_t sd_stride,
+                                          double prev, double cur, double seg) {
+  if (!(seg > kSegEps)) return -1;
+  double s0, d0, s1, d1, s2, d2;
+  lds_2f64(sd_s, s0, d0);
+  lds_2f64(sd_s + sd_stride, s1, d1);
+  lds_2f64(sd_s + 2 * sd_stride, s2, d2);
+  return exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
+}
+
+template <typename VT, int kMode>
+__device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const GridDev& g,
+                                               const double* __restrict__ tab,
+                                               double* __restrict__ rec, const Ray& r,
+                                               LeanSums& o) {
+  // next crossing parameter and smem byte address of the plane after it
+  double an0 = r.an[0], an1 = r.an[1], an2 = r.an[2];
+  const uint32_t tab_s = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
+  uint32_t qa0 = tab_s + 8u * static_cast<uint32_t>(r.q[0] + r.st[0]);
+  uint32_t qa1 = tab_s + 8u * static_cast<uint32_t>(r.q[1] + r.st[1]);
+  uint32_t qa2 = tab_s + 8u * static_cast<uint32_t>(r.q[2] + r.st[2]);
+  const int qs0 = 8 * r.st[0], qs1 = 8 * r.st[1], qs2 = 8 * r.st[2];
+  const int df0 = r.st[0], df1 = r.st[1] * g.stride[1], df2 = r.st[2] * g.stride[2];
+  // record layout: sd[a][tid] (2 doubles), inv[a][tid]
+  constexpr int nt = kLeanThreads;
+  double* sd = rec + 2 * threadIdx.x;
+  double* iv = rec + 6 * nt + threadIdx.x;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    sd[2 * a * nt] = r.s[a];
+    sd[2 * a * nt + 1] = r.d[a];
+    iv[a * nt] = r.inv[a];
+  }
+  const uint32_t sd_s = static_cast<uint32_t>(__cvta_generic_to_shared(sd));
+  const uint32_t iv_s = static_cast<uint32_t>(__cvta_generic_to_shared(iv));
+  const uint32_t sd_stride = 16u * nt, iv_stride = 8u * nt;
+  asm volatile("" ::: "memory");  // the record stores precede every record load
+  const double T2 = fmax(r.T, kSegEps);
+  const unsigned total = static_cast<unsigned>(g.total);
+  int flat = r.flat;
+  double prev = r.amin;
+  LabMask lm = lab_mask(r.lab_min);  // label of the crossing at prev
+  double pend = 0.0;
+  // Ring of kLeanPipe in-flight segments (gather issued, value consumed
+  // kLeanPipe steps later).  Steps run in blocks of kLeanPipe with the ring
+  // slot fixed at compile time, so stages never move between registers.
+  LeanStage<VT> st[kLeanPipe];
+  // one step: pick the winning crossing, consume ring slot `j` (the segment
+  // issued kLeanPipe steps ago), issue this segment's gather into slot j
+  auto step = [&](LeanStage<VT>& slot) {
+    const bool c1 = an1 < an0;  // ties go to the lowest axis (_native.pyx:180-183)
+    const double b01 = c1 ? an1 : an0;
+    const bool c2 = an2 < b01;
+    const double cur = c2 ? an2 : b01;
+    const int m2 = c2, m1 = c1 && !c2, m0 = !(c1 || c2);
+    // advance the winning axis first (its predicates die here, before the
+    // exact-path branch)
+    const double P = lds_f64(m0 * qa0 + m1 * qa1 + m2 * qa2);
+    const uint32_t k = m1 + 2 * m2;
+    double s, d;
+    lds_2f64(sd_s + k * sd_stride, s, d);
+    const double inv = lds_f64(iv_s + k * iv_stride);
+    const double an = div_rn(P - s, d, inv);
+    an0 = m0 ? an : an0;
+    an1 = m1 ? an : an1;
+    an2 = m2 ? an : an2;
+    qa0 += m0 * qs0;
+    qa1 += m1 * qs1;
+    qa2 += m2 * qs2;
+    const int flat_next = flat + m0 * df0 + m1 * df1 + m2 * df2;
+    // segment [prev, cur] in voxel `flat`
+    const double seg = cur - prev;
+    int idx = flat;
+    if (!(seg > T2) || static_cast<unsigned>(flat) >= total)
+      idx = lean_exact(g, sd_s, sd_stride, prev, cur, seg);
+    const int used = idx >= 0;
+    const VT v = gather(vol, idx, used);
+    lean_consume<kMode, VT>(o, pend, slot.seg, slot.v, slot.used, slot.m, slot.a);
+    slot.seg = seg; slot.v = v; slot.used = used; slot.m = lm; slot.a = prev;
+    lm = LabMask{m0, m1, m2};
+    prev = cur;
+    flat = flat_next;
+  };
+  const int n = r.count;
+  for (int blk = n / kLeanPipe; blk > 0; --blk) {
+#pragma unroll
+    for (int j = 0; j < kLeanPipe; ++j) step(st[j]);
+  }
+  const int rem = n % kLeanPipe;
+#pragma unroll
+  for (int j = 0; j + 1 < kLeanPipe; ++j)
+    if (j < rem) step(st[j]);
+  // drain oldest first: slots rem..PD-1 (previous block), then 0..rem-1
+#pragma unroll
+  for (int j = 0; j < kLeanPipe; ++j)
+    if (j >= rem) lean_consume<kMode, VT>(o, pend, st[j].seg, st[j].v, st[j].used, st[j].m, st[j].a);
+#pragma unroll
+  for (int j = 0; j + 1 < kLeanPipe; ++j)
+    if (j < rem) lean_consume<kMode, VT>(o, pend, st[j].seg, st[j].v, st[j].used, st[j].m, st[j].a);
+  // final segment [last crossing, amax]
+  {
+    const double cur = r.amax;
+    const double seg = cur - prev;
+    int idx = flat;
+    if (!(seg > T2) || static_cast<unsigned>(flat) >= total)
+      idx = lean_exact(g, sd_s, sd_stride, prev, cur, seg);
+    const int used = idx >= 0;
+    const VT v = gather(vol, idx, used);
+    lean_consume<kMode, VT>(o, pend, seg, v, used, lm, prev);
+  }
+  lean_finish<kMode>(o, pend, r.lab_max, r.amax);
+}
+
+// Rays with a subnormal-scale direction component (Ray::safe: |d_a| <= 1e-20,
+// never produced by a detector pose in practice) need IEEE division for their
+// crossing parameters; they take the v4 visitor walk, which has that path.
+template <typename VT, int kMode>
+__device__ __forceinline__ void safe_walk(const VT* __restrict__ vol, const GridDev& g,
+                                          const double* __restrict__ tab, const Ray& r,
+                                          LeanSums& o) {
+  if (kMode == kLeanSum) {
+    SumVisitor v;
+    walk_select<VT, true>(vol, g, tab, r, v);
+    o.acc = v.acc;
+  } else if (kMode == kLeanCount) {
+    CountVisitor v;
+    walk_select<VT, true>(vol, g, tab, r, v);
+    o.steps = v.steps;
+  } else {
+    GradVisitor v;
+    walk_select<VT, true>(vol, g, tab, r, v);
+    o.acc = v.acc;
+    o.G0 = v.G0; o.G1 = v.G1; o.G2 = v.G2;
+    o.H0 = v.H0; o.H1 = v.H1; o.H2 = v.H2;
+  }
+}
+
+template <typename VT, int kMode>
+__device__ __forceinline__ void lean_walk(const VT* __restrict__ vol, const GridDev& g,
+                                          const double* __restrict__ tab, double* rec,
+                                          const Ray& r, LeanSums& o) {
+  if (r.safe)
+    safe_walk<VT, kMode>(vol, g, tab, r, o);
+  else
+    lean_walk_impl<VT, kMode>(vol, g, tab, rec, r, o);
+}
+
+}  // namespace drr

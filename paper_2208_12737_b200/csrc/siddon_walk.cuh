@@ -97,6 +97,11 @@ constexpr int kPad = 3;
 __host__ __device__ __forceinline__ int plane_table_len(const GridDev& g) {
   return g.n[0] + g.n[1] + g.n[2] + 3 * (2 * kPad + 1);
 }
+// Start of the per-thread area after the plane table, in doubles: rounded up
+// to an even count so 16-byte shared-memory vector loads stay aligned.
+__host__ __device__ __forceinline__ int plane_table_span(const GridDev& g) {
+  return (plane_table_len(g) + 1) & ~1;
+}
 __host__ __device__ __forceinline__ int plane_base(const GridDev& g, int a) {
   return a == 0 ? kPad
                 : (a == 1 ? g.n[0] + 1 + 3 * kPad : g.n[0] + g.n[1] + 2 + 5 * kPad);
@@ -131,6 +136,7 @@ struct Ray {
   int end_lab;      // chunked walk: crossings tied with amax on axes >= end_lab
                     // belong to the next chunk (kNoEndLab for a ray's real exit)
   int flat;         // flat voxel index of the segment after amin
+  int count;        // crossings this walk takes (the counted walk, siddon_lean.cuh)
   bool hit;
   bool safe;        // some |d_a| tiny: use IEEE '/' instead of the Markstein form
 };
@@ -294,6 +300,7 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
     }
   }
   int vox[3];
+  r.count = 0;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     if (r.st[a] == 0) {
@@ -316,6 +323,11 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
     r.q[a] = plane_base(g, a) + k;
     r.an[a] = (k >= 0 && k <= n) ? axis_alpha(g, r, a, k) : kSentinel;
     vox[a] = r.st[a] > 0 ? k - 1 : k;
+    // crossings of axis a this walk takes: after the start event (k on) and
+    // up to the end event -- alpha <= amax, or alpha < amax for axes >= end_lab
+    const int k_end = first_plane_after(g, r, a, r.amax, a < r.end_lab);
+    const int c = (k_end - k) * r.st[a];
+    r.count += c > 0 ? c : 0;
   }
   r.flat = vox[0] + g.stride[1] * vox[1] + g.stride[2] * vox[2];
 }
