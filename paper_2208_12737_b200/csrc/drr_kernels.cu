@@ -563,6 +563,7 @@ __global__ void __launch_bounds__(kRayThreads)
 }  // namespace drr
 
 // =================================================================== C ABI
+#ifndef DRR_KERNELS_ONLY  // (scripts/sass_harness.cu compiles single kernels for SASS study)
 namespace {
 
 thread_local char g_err[512] = "";
@@ -1042,3 +1043,4 @@ int drr_register_update(double* d_eta, double* d_velocity, const double* d_grad_
 }
 
 }  // extern "C"
+#endif  // DRR_KERNELS_ONLY

@@ -33,7 +33,7 @@ constexpr int kLeanThreads = 128;  // threads per CTA of every kernel using the 
 // after its load is issued (ncu lean1: 45% of stall samples waited on the
 // gather when it was consumed one step later).
 #ifndef DRR_LEAN_PIPE
-#define DRR_LEAN_PIPE 3
+#define DRR_LEAN_PIPE 4
 #endif
 constexpr int kLeanPipe = DRR_LEAN_PIPE;
 
@@ -45,23 +45,35 @@ struct LeanSums {
   int steps = 0;
 };
 
-// One-hot axis masks of a crossing label (label 3 = clip: all zero, no
-// tangent), as 0/1 integers.
+// Label of a crossing as the high words of three 0.0/1.0 doubles (one-hot over
+// the axes; label 3 = clip: all zero, no tangent).
 struct LabMask {
-  int m0, m1, m2;
+  int h0, h1, h2;
 };
+constexpr int kOneHi = 0x3FF00000;  // high word of 1.0
 __device__ __forceinline__ LabMask lab_mask(int lab) {
-  return LabMask{lab == 0, lab == 1, lab == 2};
+  return LabMask{lab == 0 ? kOneHi : 0, lab == 1 ? kOneHi : 0, lab == 2 ? kOneHi : 0};
 }
-// 0.0 / 1.0 from a 0/1 mask (high word only, on the integer FMA pipe)
-__device__ __forceinline__ double mask_d(int m) { return __hiloint2double(m * 0x3FF00000, 0); }
 
-// G_lab += c and H_lab += c * alpha as masked FMAs: no per-lane branch and no
-// select tree (c * 1 and c * 0 are exact; H rounds c * alpha once before the
-// add, ~1 ulp of one term -- the oracle comparison bar is 1e-10 relative).
+// A segment whose gather is in flight: the parameter of its starting crossing
+// (its length is the next stage's parameter minus this one -- the same
+// subtraction the walk made, so bit-identical), the value (0 if skipped), the
+// starting crossing's label and, for counting, the used flag.
+template <typename VT>
+struct LeanStage {
+  double a = 0.0;
+  VT v = VT(0);
+  LabMask m{0, 0, 0};
+  int used = 0;
+};
+
+// G_lab += c and H_lab += c * alpha as FMAs by 0.0/1.0 masks: no per-lane
+// branch and no select tree (c * 1 and c * 0 are exact; H rounds c * alpha
+// once before the add, ~1 ulp of one term; the oracle bar is 1e-10 relative).
 __device__ __forceinline__ void lean_apply(LeanSums& o, const LabMask& m, double a, double c) {
   const double ca = c * a;
-  const double k0 = mask_d(m.m0), k1 = mask_d(m.m1), k2 = mask_d(m.m2);
+  const double k0 = __hiloint2double(m.h0, 0), k1 = __hiloint2double(m.h1, 0),
+               k2 = __hiloint2double(m.h2, 0);
   o.G0 = __fma_rn(c, k0, o.G0);
   o.G1 = __fma_rn(c, k1, o.G1);
   o.G2 = __fma_rn(c, k2, o.G2);
@@ -70,27 +82,19 @@ __device__ __forceinline__ void lean_apply(LeanSums& o, const LabMask& m, double
   o.H2 = __fma_rn(ca, k2, o.H2);
 }
 
-// A segment whose gather is in flight: length, value (0 if unused), the
-// used flag, and the label mask and parameter of its starting crossing.
-template <typename VT>
-struct LeanStage {
-  double seg = 0.0, a = 0.0;
-  VT v = VT(0);
-  int used = 0;
-  LabMask m{0, 0, 0};
-};
-
+// Consume one segment: [a, a_next) with value v.
 template <int kMode, typename VT>
-__device__ __forceinline__ void lean_consume(LeanSums& o, double& pend, double seg, VT v,
-                                             int used, const LabMask& m, double a) {
+__device__ __forceinline__ void lean_consume(LeanSums& o, double& pend, const LeanStage<VT>& st,
+                                             double a_next) {
   if (kMode == kLeanCount) {
-    o.steps += used;
+    o.steps += st.used;
     return;
   }
-  const double vv = static_cast<double>(v);  // 0 for unused segments
-  o.acc = o.acc + seg * vv;                    // _native.pyx:187 (TU is --fmad=false)
+  const double vv = static_cast<double>(st.v);  // 0 for skipped segments
+  const double seg = a_next - st.a;
+  o.acc = o.acc + seg * vv;                       // _native.pyx:187 (TU is --fmad=false)
   if (kMode == kLeanGrad) {
-    lean_apply(o, m, a, pend - vv);
+    lean_apply(o, st.m, st.a, pend - vv);
     pend = vv;
   }
 }
@@ -109,34 +113,24 @@ __device__ __forceinline__ void lds_2f64(uint32_t addr, double& a, double& b) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr));
 }
 
-// Predicated gather: v = used ? vol[idx] : 0, with no branch around the load
-// (so nothing in this iteration depends on its arrival).
-__device__ __forceinline__ float gather(const float* __restrict__ vol, int idx, int used) {
-  float v;
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %2, 0;\n\tmov.b32 %0, 0;\n\t"
-               "@p ld.global.nc.f32 %0, [%1];\n\t}"
-               : "=f"(v) : "l"(vol + idx), "r"(used));
-  return v;
-}
-__device__ __forceinline__ double gather(const double* __restrict__ vol, int idx, int used) {
-  double v;
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %2, 0;\n\tmov.b64 %0, 0;\n\t"
-               "@p ld.global.nc.f64 %0, [%1];\n\t}"
-               : "=d"(v) : "l"(vol + idx), "r"(used));
-  return v;
-}
+// Skipped segments gather from here (a zero, so they add nothing and need no
+// predicate on the load).
+__device__ const double g_zero_voxel = 0.0;
 
 // Exact path (out of the fast path): the used test and the reference's
 // floored midpoint (_native.pyx:68-82, 186), with s and d from the record.
-// Returns the voxel, or -1 for a skipped segment.
-__device__ __forceinline__ int lean_exact(const GridDev& g, uint32_t sd_s, uint32_t sd_stride,
-                                          double prev, double cur, double seg) {
-  if (!(seg > kSegEps)) return -1;
+// Returns the address to gather (the zero voxel for a skipped segment).
+template <typename VT>
+__device__ __forceinline__ const VT* lean_exact(const VT* __restrict__ vol, const GridDev& g,
+                                                uint32_t sd_s, uint32_t sd_stride, double prev,
+                                                double cur, double seg, int& used) {
+  used = seg > kSegEps;
+  if (!used) return reinterpret_cast<const VT*>(&g_zero_voxel);
   double s0, d0, s1, d1, s2, d2;
   lds_2f64(sd_s, s0, d0);
   lds_2f64(sd_s + sd_stride, s1, d1);
   lds_2f64(sd_s + 2 * sd_stride, s2, d2);
-  return exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
+  return vol + exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
 }
 
 template <typename VT, int kMode>
@@ -151,7 +145,12 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   uint32_t qa1 = tab_s + 8u * static_cast<uint32_t>(r.q[1] + r.st[1]);
   uint32_t qa2 = tab_s + 8u * static_cast<uint32_t>(r.q[2] + r.st[2]);
   const int qs0 = 8 * r.st[0], qs1 = 8 * r.st[1], qs2 = 8 * r.st[2];
-  const int df0 = r.st[0], df1 = r.st[1] * g.stride[1], df2 = r.st[2] * g.stride[2];
+  // voxel bookkeeping as a byte pointer (a certified segment's voxel is in
+  // range: its midpoint is more than the rounding noise inside every slab)
+  const int db0 = r.st[0] * static_cast<int>(sizeof(VT)),
+            db1 = r.st[1] * g.stride[1] * static_cast<int>(sizeof(VT)),
+            db2 = r.st[2] * g.stride[2] * static_cast<int>(sizeof(VT));
+  const char* bp = reinterpret_cast<const char*>(vol + r.flat);
   // record layout: sd[a][tid] (2 doubles), inv[a][tid]
   constexpr int nt = kLeanThreads;
   double* sd = rec + 2 * threadIdx.x;
@@ -164,28 +163,30 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   }
   const uint32_t sd_s = static_cast<uint32_t>(__cvta_generic_to_shared(sd));
   const uint32_t iv_s = static_cast<uint32_t>(__cvta_generic_to_shared(iv));
-  const uint32_t sd_stride = 16u * nt, iv_stride = 8u * nt;
+  constexpr uint32_t sd_stride = 16u * nt, iv_stride = 8u * nt;
   asm volatile("" ::: "memory");  // the record stores precede every record load
   const double T2 = fmax(r.T, kSegEps);
-  const unsigned total = static_cast<unsigned>(g.total);
-  int flat = r.flat;
   double prev = r.amin;
   LabMask lm = lab_mask(r.lab_min);  // label of the crossing at prev
   double pend = 0.0;
   // Ring of kLeanPipe in-flight segments (gather issued, value consumed
   // kLeanPipe steps later).  Steps run in blocks of kLeanPipe with the ring
   // slot fixed at compile time, so stages never move between registers.
+  // Initially every slot is an empty segment [amin, amin) (adds nothing).
   LeanStage<VT> st[kLeanPipe];
-  // one step: pick the winning crossing, consume ring slot `j` (the segment
-  // issued kLeanPipe steps ago), issue this segment's gather into slot j
-  auto step = [&](LeanStage<VT>& slot) {
+#pragma unroll
+  for (int j = 0; j < kLeanPipe; ++j) st[j].a = prev;
+  // one step: consume ring slot j (the segment issued kLeanPipe steps ago;
+  // it ends where slot j+1's segment starts), pick the winning crossing,
+  // issue this segment's gather into slot j
+  auto step = [&](int j) {
+    lean_consume<kMode, VT>(o, pend, st[j], st[(j + 1) % kLeanPipe].a);
     const bool c1 = an1 < an0;  // ties go to the lowest axis (_native.pyx:180-183)
     const double b01 = c1 ? an1 : an0;
     const bool c2 = an2 < b01;
     const double cur = c2 ? an2 : b01;
     const int m2 = c2, m1 = c1 && !c2, m0 = !(c1 || c2);
-    // advance the winning axis first (its predicates die here, before the
-    // exact-path branch)
+    // advance the winning axis
     const double P = lds_f64(m0 * qa0 + m1 * qa1 + m2 * qa2);
     const uint32_t k = m1 + 2 * m2;
     double s, d;
@@ -198,46 +199,51 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     qa0 += m0 * qs0;
     qa1 += m1 * qs1;
     qa2 += m2 * qs2;
-    const int flat_next = flat + m0 * df0 + m1 * df1 + m2 * df2;
-    // segment [prev, cur] in voxel `flat`
+    // segment [prev, cur] in the bookkeeping voxel
+    const VT* gp = reinterpret_cast<const VT*>(bp);
+    int used = 1;
     const double seg = cur - prev;
-    int idx = flat;
-    if (!(seg > T2) || static_cast<unsigned>(flat) >= total)
-      idx = lean_exact(g, sd_s, sd_stride, prev, cur, seg);
-    const int used = idx >= 0;
-    const VT v = gather(vol, idx, used);
-    lean_consume<kMode, VT>(o, pend, slot.seg, slot.v, slot.used, slot.m, slot.a);
-    slot.seg = seg; slot.v = v; slot.used = used; slot.m = lm; slot.a = prev;
-    lm = LabMask{m0, m1, m2};
+    if (!(seg > T2)) gp = lean_exact(vol, g, sd_s, sd_stride, prev, cur, seg, used);
+    bp += m0 * db0 + m1 * db1 + m2 * db2;
+    st[j].v = __ldg(gp);
+    st[j].used = used;
+    st[j].a = prev;
+    st[j].m = lm;
+    lm = LabMask{m0 * kOneHi, m1 * kOneHi, m2 * kOneHi};
     prev = cur;
-    flat = flat_next;
   };
   const int n = r.count;
   for (int blk = n / kLeanPipe; blk > 0; --blk) {
 #pragma unroll
-    for (int j = 0; j < kLeanPipe; ++j) step(st[j]);
+    for (int j = 0; j < kLeanPipe; ++j) step(j);
   }
   const int rem = n % kLeanPipe;
 #pragma unroll
   for (int j = 0; j + 1 < kLeanPipe; ++j)
-    if (j < rem) step(st[j]);
-  // drain oldest first: slots rem..PD-1 (previous block), then 0..rem-1
+    if (j < rem) step(j);
+  // drain oldest first: slots rem..PD-1 (previous block), then 0..rem-1; each
+  // ends where the next-younger one starts, the youngest at prev
 #pragma unroll
   for (int j = 0; j < kLeanPipe; ++j)
-    if (j >= rem) lean_consume<kMode, VT>(o, pend, st[j].seg, st[j].v, st[j].used, st[j].m, st[j].a);
+    if (j >= rem)
+      lean_consume<kMode, VT>(o, pend, st[j],
+                              j + 1 < kLeanPipe ? st[j + 1].a : (rem > 0 ? st[0].a : prev));
 #pragma unroll
   for (int j = 0; j + 1 < kLeanPipe; ++j)
-    if (j < rem) lean_consume<kMode, VT>(o, pend, st[j].seg, st[j].v, st[j].used, st[j].m, st[j].a);
+    if (j < rem) lean_consume<kMode, VT>(o, pend, st[j], j + 1 < rem ? st[j + 1].a : prev);
   // final segment [last crossing, amax]
   {
     const double cur = r.amax;
     const double seg = cur - prev;
-    int idx = flat;
-    if (!(seg > T2) || static_cast<unsigned>(flat) >= total)
-      idx = lean_exact(g, sd_s, sd_stride, prev, cur, seg);
-    const int used = idx >= 0;
-    const VT v = gather(vol, idx, used);
-    lean_consume<kMode, VT>(o, pend, seg, v, used, lm, prev);
+    const VT* gp = reinterpret_cast<const VT*>(bp);
+    int used = 1;
+    if (!(seg > T2)) gp = lean_exact(vol, g, sd_s, sd_stride, prev, cur, seg, used);
+    LeanStage<VT> last;
+    last.a = prev;
+    last.v = __ldg(gp);
+    last.used = used;
+    last.m = lm;
+    lean_consume<kMode, VT>(o, pend, last, cur);
   }
   lean_finish<kMode>(o, pend, r.lab_max, r.amax);
 }
