@@ -39,12 +39,12 @@ namespace drr {
 #else
 #define DRR_LB __launch_bounds__(kThreads)
 #endif
-// Launch bounds (A/B on C2, 32 poses, walk v5 with a 3-deep gather pipeline):
-// the gradient walks (k_forward_jac, k_backward) at 4 CTAs/SM (<= 128
-// registers, no spills) and the forward at 6 CTAs/SM (<= 80) beat 5 and 8
-// CTAs/SM, where ptxas spilled: 3.08 vs 3.74 ms and 2.19 vs 2.56 ms.
+// Launch bounds (A/B on C2, 32 poses, walk v6; scripts/gpu_ab.sh): the
+// gradient walks (k_forward_jac, k_backward) at 5 CTAs/SM with a 3-deep
+// gather pipeline and the forward at 6 CTAs/SM with a 4-deep one were the
+// fastest of the spill-free combinations (2.64 ms / 2.0 ms for 32 poses).
 #ifndef DRR_BWD_MINB
-#define DRR_BWD_MINB 4
+#define DRR_BWD_MINB 5
 #endif
 #ifndef DRR_FWD_MINB
 #define DRR_FWD_MINB 6

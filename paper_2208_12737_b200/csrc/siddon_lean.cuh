@@ -27,15 +27,28 @@ namespace drr {
 
 // Per-thread shared-memory record: {s_a, d_a} (16 B) and 1/d_a (8 B) per
 // axis, structure-of-arrays over the CTA's threads (conflict-free LDS.128).
-constexpr int kLeanRecDoublesPerThread = 9;
-constexpr int kLeanThreads = 128;  // threads per CTA of every kernel using the walk
-// Gather pipeline depth: a segment's voxel value is consumed kLeanPipe steps
-// after its load is issued (ncu lean1: 45% of stall samples waited on the
-// gather when it was consumed one step later).
-#ifndef DRR_LEAN_PIPE
-#define DRR_LEAN_PIPE 4
+// Walk tuning, per mode (A/B on C2, see profiles/):
+//  * kQ: the record also holds each axis's plane-table cursor and its strides
+//    ({1/d, table step, voxel byte step} 16 B, cursor 4 B), so the winner's
+//    bookkeeping is one record load and one store instead of per-axis selects
+//    (fewer ALU/issue slots, more shared-memory wavefronts);
+//  * PD: gather pipeline depth -- a segment's voxel value is consumed PD steps
+//    after its load is issued (ncu lean1: 45% of stall samples waited on the
+//    gather when it was consumed one step later).
+#ifndef DRR_LEAN_PIPE_FWD
+#define DRR_LEAN_PIPE_FWD 4
 #endif
-constexpr int kLeanPipe = DRR_LEAN_PIPE;
+#ifndef DRR_LEAN_PIPE_GRAD
+#define DRR_LEAN_PIPE_GRAD 3
+#endif
+#ifndef DRR_LEAN_Q_FWD
+#define DRR_LEAN_Q_FWD 0
+#endif
+#ifndef DRR_LEAN_Q_GRAD
+#define DRR_LEAN_Q_GRAD 1
+#endif
+constexpr int kLeanRecDoublesPerThread = 14;
+constexpr int kLeanThreads = 128;  // threads per CTA of every kernel using the walk
 
 enum LeanMode { kLeanSum = 0, kLeanCount = 1, kLeanGrad = 2 };
 
@@ -133,7 +146,7 @@ __device__ __forceinline__ const VT* lean_exact(const VT* __restrict__ vol, cons
   return vol + exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
 }
 
-template <typename VT, int kMode>
+template <typename VT, int kMode, int kLeanPipe, bool kQ>
 __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const GridDev& g,
                                                const double* __restrict__ tab,
                                                double* __restrict__ rec, const Ray& r,
@@ -141,29 +154,48 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   // next crossing parameter and smem byte address of the plane after it
   double an0 = r.an[0], an1 = r.an[1], an2 = r.an[2];
   const uint32_t tab_s = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
-  uint32_t qa0 = tab_s + 8u * static_cast<uint32_t>(r.q[0] + r.st[0]);
-  uint32_t qa1 = tab_s + 8u * static_cast<uint32_t>(r.q[1] + r.st[1]);
-  uint32_t qa2 = tab_s + 8u * static_cast<uint32_t>(r.q[2] + r.st[2]);
-  const int qs0 = 8 * r.st[0], qs1 = 8 * r.st[1], qs2 = 8 * r.st[2];
+  const uint32_t qa_init[3] = {tab_s + 8u * static_cast<uint32_t>(r.q[0] + r.st[0]),
+                               tab_s + 8u * static_cast<uint32_t>(r.q[1] + r.st[1]),
+                               tab_s + 8u * static_cast<uint32_t>(r.q[2] + r.st[2])};
+  const int db_init[3] = {r.st[0] * static_cast<int>(sizeof(VT)),
+                          r.st[1] * g.stride[1] * static_cast<int>(sizeof(VT)),
+                          r.st[2] * g.stride[2] * static_cast<int>(sizeof(VT))};
   // voxel bookkeeping as a byte pointer (a certified segment's voxel is in
   // range: its midpoint is more than the rounding noise inside every slab)
-  const int db0 = r.st[0] * static_cast<int>(sizeof(VT)),
-            db1 = r.st[1] * g.stride[1] * static_cast<int>(sizeof(VT)),
-            db2 = r.st[2] * g.stride[2] * static_cast<int>(sizeof(VT));
   const char* bp = reinterpret_cast<const char*>(vol + r.flat);
-  // record layout: sd[a][tid] (2 doubles), inv[a][tid]
+  // record layout (structure of arrays over the CTA's threads):
+  //   sd[a][tid] = {s_a, d_a}; iv[a][tid] = 1/d_a (+ table step, voxel byte
+  //   step when kQ); qc[a][tid] = table cursor (kQ)
   constexpr int nt = kLeanThreads;
   double* sd = rec + 2 * threadIdx.x;
-  double* iv = rec + 6 * nt + threadIdx.x;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     sd[2 * a * nt] = r.s[a];
     sd[2 * a * nt + 1] = r.d[a];
-    iv[a * nt] = r.inv[a];
   }
   const uint32_t sd_s = static_cast<uint32_t>(__cvta_generic_to_shared(sd));
+  constexpr uint32_t sd_stride = 16u * nt;
+  // (kQ) iv[a][tid] = {1/d, table step, voxel byte step}, qc[a][tid] = cursor;
+  // (!kQ) iv[a][tid] = 1/d, cursors and steps in registers
+  uint32_t qa0 = qa_init[0], qa1 = qa_init[1], qa2 = qa_init[2];
+  const int qs0 = 8 * r.st[0], qs1 = 8 * r.st[1], qs2 = 8 * r.st[2];
+  const int db0 = db_init[0], db1 = db_init[1], db2 = db_init[2];
+  double* iv = rec + 6 * nt + (kQ ? 2 : 1) * threadIdx.x;
+  uint32_t* qc = reinterpret_cast<uint32_t*>(rec + 12 * nt) + threadIdx.x;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if constexpr (kQ) {
+      iv[2 * a * nt] = r.inv[a];
+      reinterpret_cast<int*>(iv + 2 * a * nt + 1)[0] = 8 * r.st[a];
+      reinterpret_cast<int*>(iv + 2 * a * nt + 1)[1] = db_init[a];
+      qc[a * nt] = qa_init[a];
+    } else {
+      iv[a * nt] = r.inv[a];
+    }
+  }
   const uint32_t iv_s = static_cast<uint32_t>(__cvta_generic_to_shared(iv));
-  constexpr uint32_t sd_stride = 16u * nt, iv_stride = 8u * nt;
+  const uint32_t qc_s = static_cast<uint32_t>(__cvta_generic_to_shared(qc));
+  constexpr uint32_t iv_stride = (kQ ? 16u : 8u) * nt, qc_stride = 4u * nt;
   asm volatile("" ::: "memory");  // the record stores precede every record load
   const double T2 = fmax(r.T, kSegEps);
   double prev = r.amin;
@@ -187,24 +219,39 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     const double cur = c2 ? an2 : b01;
     const int m2 = c2, m1 = c1 && !c2, m0 = !(c1 || c2);
     // advance the winning axis
-    const double P = lds_f64(m0 * qa0 + m1 * qa1 + m2 * qa2);
     const uint32_t k = m1 + 2 * m2;
     double s, d;
     lds_2f64(sd_s + k * sd_stride, s, d);
-    const double inv = lds_f64(iv_s + k * iv_stride);
+    double inv, P;
+    int db;
+    if constexpr (kQ) {
+      long long steps;  // {table step (low word), voxel byte step (high word)}
+      asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=d"(inv), "=l"(steps)
+                   : "r"(iv_s + k * iv_stride));
+      const int qs = static_cast<int>(steps);
+      db = static_cast<int>(steps >> 32);
+      uint32_t qa;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(qa) : "r"(qc_s + k * qc_stride));
+      P = lds_f64(qa);
+      asm volatile("st.shared.u32 [%0], %1;" :: "r"(qc_s + k * qc_stride), "r"(qa + qs) : "memory");
+    } else {
+      P = lds_f64(m0 * qa0 + m1 * qa1 + m2 * qa2);
+      inv = lds_f64(iv_s + k * iv_stride);
+      qa0 += m0 * qs0;
+      qa1 += m1 * qs1;
+      qa2 += m2 * qs2;
+      db = m0 * db0 + m1 * db1 + m2 * db2;
+    }
     const double an = div_rn(P - s, d, inv);
     an0 = m0 ? an : an0;
     an1 = m1 ? an : an1;
     an2 = m2 ? an : an2;
-    qa0 += m0 * qs0;
-    qa1 += m1 * qs1;
-    qa2 += m2 * qs2;
     // segment [prev, cur] in the bookkeeping voxel
     const VT* gp = reinterpret_cast<const VT*>(bp);
     int used = 1;
     const double seg = cur - prev;
     if (!(seg > T2)) gp = lean_exact(vol, g, sd_s, sd_stride, prev, cur, seg, used);
-    bp += m0 * db0 + m1 * db1 + m2 * db2;
+    bp += db;
     st[j].v = __ldg(gp);
     st[j].used = used;
     st[j].a = prev;
@@ -279,7 +326,8 @@ __device__ __forceinline__ void lean_walk(const VT* __restrict__ vol, const Grid
   if (r.safe)
     safe_walk<VT, kMode>(vol, g, tab, r, o);
   else
-    lean_walk_impl<VT, kMode>(vol, g, tab, rec, r, o);
+    lean_walk_impl<VT, kMode, kMode == kLeanGrad ? DRR_LEAN_PIPE_GRAD : DRR_LEAN_PIPE_FWD,
+                   kMode == kLeanGrad ? DRR_LEAN_Q_GRAD : DRR_LEAN_Q_FWD>(vol, g, tab, rec, r, o);
 }
 
 }  // namespace drr
