@@ -56,14 +56,20 @@ constexpr int kThreads = 128;  // 4 warps per CTA
 constexpr int kFrameGrads = 12;
 
 // CTA pixel tile for K threads per ray (SURVEY 7 H2 ray splitting):
-//   K = 1: 16 x 8 pixels, each warp an 8 x 4 quad (neighbouring rays share
-//          L1/L2 lines of the CT);
+//   K = 1: each warp a kQuadW x (32 / kQuadW) quad of adjacent pixels
+//          (neighbouring rays share L1/L2 lines of the CT), the CTA 2 x 2
+//          quads (4 x 1 when kQuadW = 32);
 //   K > 1: 128 / K rays as an 8 x (16 / K) tile; the K chunks of a ray are K
 //          consecutive lanes of one warp, combined with xor shuffles.
+#ifndef DRR_QUAD_W
+#define DRR_QUAD_W 8
+#endif
+constexpr int kQuadW = DRR_QUAD_W, kQuadH = 32 / kQuadW;
+constexpr int kCtaQuadsW = kQuadW == 32 ? 1 : 2, kCtaQuadsH = 4 / kCtaQuadsW;
 template <int K>
 struct Tile {
-  static constexpr int W = K == 1 ? 16 : 8;
-  static constexpr int H = K == 1 ? 8 : 16 / K;
+  static constexpr int W = K == 1 ? kQuadW * kCtaQuadsW : 8;
+  static constexpr int H = K == 1 ? kQuadH * kCtaQuadsH : 16 / K;
 };
 
 template <int K>
@@ -71,8 +77,8 @@ __device__ __forceinline__ void tile_ray(int& h, int& w, int& chunk) {
   const int t = threadIdx.x;
   if (K == 1) {
     const int warp = t >> 5, lane = t & 31;
-    w = blockIdx.x * Tile<K>::W + (warp & 1) * 8 + (lane & 7);
-    h = blockIdx.y * Tile<K>::H + (warp >> 1) * 4 + (lane >> 3);
+    w = blockIdx.x * Tile<K>::W + (warp % kCtaQuadsW) * kQuadW + (lane % kQuadW);
+    h = blockIdx.y * Tile<K>::H + (warp / kCtaQuadsW) * kQuadH + (lane / kQuadW);
     chunk = 0;
   } else {
     const int ray = t / K;
