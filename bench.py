@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--batch", type=int, default=32, help="poses per GPU per step")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-other-configs", action="store_true",
+                   help="skip the C1/C4/C5 context measurements")
     p.add_argument("--cpu-sample", type=int, default=0, help="poses for the CPU baseline (0: auto)")
     return p.parse_args()
 
@@ -182,6 +184,66 @@ def cpu_model():
 
 
 # ------------------------------------------------------------------- main
+# ------------------------------------------------- the other BASELINE configs
+def other_configs(dev, vol_c2, timed_fn, flush):
+    """C1 / C4 / C5 of BASELINE.json measured on this GPU (rank 0, N=1; they are
+    parity-test cases in tests/test_gpu_configs.py, reported here for context,
+    not the headline).  Device time with CUDA events, L2 flushed between reps."""
+    import torch
+    from paper_2208_12737_b200 import (DeviceVolume, Detector, backward_from_jac, count_steps,
+                                       pose_frames, render_frames, render_frames_jac, synthetic)
+    out = {}
+    # C1: 128^3 sphere @ 1 mm, 100^2 @ 2.56 mm, one oblique pose, forward only
+    v1 = DeviceVolume(synthetic.make_phantom("sphere", 128, 1.0), 1.0, device=dev)
+    d1 = Detector(100, 100, 2.56)
+    f1 = pose_frames(torch.tensor([[300.0, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0]], device=dev),
+                     v1.center).detach()
+    t = timed_fn(lambda: render_frames(v1, d1, f1), 20, 3)
+    out["C1"] = {"workload": "128^3 sphere @1 mm, 100x100 @2.56 mm, 1 pose, forward",
+                 "ms_per_drr": float(np.median(t))}
+    # C4: C2 volume, 1024 narrow poses (seed 0), 256^2 @ 2.8125 mm, forward only
+    d4 = Detector(256, 256, 2.8125)
+    p4 = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, 1024, seed=0)
+    f4 = pose_frames(torch.tensor(p4, device=dev), vol_c2.center).detach()
+    t = timed_fn(lambda: render_frames(vol_c2, d4, f4), 5, 2)
+    S4 = float(count_steps(vol_c2, d4, f4[:128].contiguous()).double().sum()) / 128
+    out["C4"] = {"workload": "C2 volume, 1024 narrow poses seed 0, 256x256 @2.8125 mm, forward, "
+                             "one launch (per-GPU shard at N=1)",
+                 "ms_per_batch": float(np.median(t)), "drr_per_s": 1024 / (float(np.median(t)) / 1e3),
+                 "voxel_steps_per_drr": S4}
+    # C5: 512^3 @ 0.703125 (sphere + 3x off-centre cube + noise), 1024^2 @ 0.703125,
+    # forward + backward; 16 poses per launch (the Jacobian of 16 poses is 0.8 GB)
+    n = 512
+    c = (torch.arange(n, device=dev, dtype=torch.float64) + 0.5) * 0.703125
+    mid, rad = n * 0.703125 / 2, 0.4 * n * 0.703125
+    r2 = (c - mid)[:, None, None] ** 2 + (c - mid)[None, :, None] ** 2 + (c - mid)[None, None, :] ** 2
+    frac = (torch.arange(n, device=dev, dtype=torch.float64) + 0.5) / n
+    inb = (frac >= 0.25) & (frac <= 0.5)
+    v5 = (r2 <= rad * rad).double() + 3.0 * (inb[:, None, None] & inb[None, :, None] & inb[None, None, :]).double()
+    gen = torch.Generator(device=dev).manual_seed(5)
+    v5 = torch.clamp(v5 + 0.01 * torch.randn(v5.shape, device=dev, generator=gen, dtype=torch.float64)
+                     * (v5 > 0), min=0.0).float()
+    vol5 = DeviceVolume(v5, 0.703125, device=dev)
+    del v5, r2
+    d5 = Detector(1024, 1024, 0.703125)
+    p5 = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, 16, seed=0)
+    f5 = pose_frames(torch.tensor(p5, device=dev), vol5.center).detach()
+    g5 = torch.randn((16, 1024, 1024), device=dev)
+    hold = {}
+
+    def c5_step():
+        hold["img"], hold["jac"] = render_frames_jac(vol5, d5, f5)
+        backward_from_jac(d5, hold["jac"], g5)
+
+    t = timed_fn(c5_step, 3, 1)
+    out["C5"] = {"workload": "512^3 @0.703125 sphere+3x cube+noise, 1024x1024 @0.703125, "
+                             "16 poses per launch, forward + backward (one walk + contraction)",
+                 "ms_per_batch": float(np.median(t)), "drr_per_s": 16 / (float(np.median(t)) / 1e3)}
+    del vol5, hold
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -422,6 +484,8 @@ def main():
                             "final_neg_zncc": reg_final, "cuda_graph": True},
         "clocks": clocks,
     }
+    if world == 1 and not args.no_other_configs:
+        result["other_configs"] = other_configs(dev, drr.volume, timed, flush)
     if not args.no_cpu_baseline and world == 1:
         vol_np = vol_np if vol_np is not None else synthetic.chest_phantom(DIMS)
         kind, worker, fixed_np = cpu_setup(vol_np)
