@@ -58,6 +58,19 @@ struct LeanSums {
   int steps = 0;
 };
 
+// Derived dominant axis (gradient walk, DRR_LEAN_DERIVE): over all crossings
+// of a walk -- entry and exit included -- the coefficients telescope,
+// sum_k c_k = 0, and sum_k c_k alpha_k = sum_m V_m seg_m = acc (Abel
+// summation).  So only the two non-dominant axes A, B are accumulated per
+// step (masks A, B; slots G0/H0, G1/H1) and the dominant axis D follows at the
+// end: G_D = -(G_A + G_B + G_clip), H_D = acc - H_A - H_B - H_clip, where the
+// clip terms come from a clip-labelled exit (a clip entry takes the 3-axis
+// walk).  |d_D| >= |d| / sqrt(3), so the rounding of the derived H_D (a few
+// ulps of acc) is not amplified by the 1/d_D of the endpoint formula.
+#ifndef DRR_LEAN_DERIVE
+#define DRR_LEAN_DERIVE 1
+#endif
+
 // Label of a crossing as the high words of three 0.0/1.0 doubles (one-hot over
 // the axes; label 3 = clip: all zero, no tangent).
 struct LabMask {
@@ -83,20 +96,23 @@ struct LeanStage {
 // G_lab += c and H_lab += c * alpha as FMAs by 0.0/1.0 masks: no per-lane
 // branch and no select tree (c * 1 and c * 0 are exact; H rounds c * alpha
 // once before the add, ~1 ulp of one term; the oracle bar is 1e-10 relative).
+template <bool kDerive>
 __device__ __forceinline__ void lean_apply(LeanSums& o, const LabMask& m, double a, double c) {
   const double ca = c * a;
-  const double k0 = __hiloint2double(m.h0, 0), k1 = __hiloint2double(m.h1, 0),
-               k2 = __hiloint2double(m.h2, 0);
+  const double k0 = __hiloint2double(m.h0, 0), k1 = __hiloint2double(m.h1, 0);
   o.G0 = __fma_rn(c, k0, o.G0);
   o.G1 = __fma_rn(c, k1, o.G1);
-  o.G2 = __fma_rn(c, k2, o.G2);
   o.H0 = __fma_rn(ca, k0, o.H0);
   o.H1 = __fma_rn(ca, k1, o.H1);
-  o.H2 = __fma_rn(ca, k2, o.H2);
+  if constexpr (!kDerive) {
+    const double k2 = __hiloint2double(m.h2, 0);
+    o.G2 = __fma_rn(c, k2, o.G2);
+    o.H2 = __fma_rn(ca, k2, o.H2);
+  }
 }
 
 // Consume one segment: [a, a_next) with value v.
-template <int kMode, typename VT>
+template <int kMode, bool kDerive, typename VT>
 __device__ __forceinline__ void lean_consume(LeanSums& o, double& pend, const LeanStage<VT>& st,
                                              double a_next) {
   if (kMode == kLeanCount) {
@@ -107,14 +123,9 @@ __device__ __forceinline__ void lean_consume(LeanSums& o, double& pend, const Le
   const double seg = a_next - st.a;
   o.acc = o.acc + seg * vv;                       // _native.pyx:187 (TU is --fmad=false)
   if (kMode == kLeanGrad) {
-    lean_apply(o, st.m, st.a, pend - vv);
+    lean_apply<kDerive>(o, st.m, st.a, pend - vv);
     pend = vv;
   }
-}
-
-template <int kMode>
-__device__ __forceinline__ void lean_finish(LeanSums& o, double pend, int lab, double a) {
-  if (kMode == kLeanGrad) lean_apply(o, lab_mask(lab), a, pend);
 }
 
 __device__ __forceinline__ double lds_f64(uint32_t addr) {
@@ -146,7 +157,7 @@ __device__ __forceinline__ const VT* lean_exact(const VT* __restrict__ vol, cons
   return vol + exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
 }
 
-template <typename VT, int kMode, int kLeanPipe, bool kQ>
+template <typename VT, int kMode, int kLeanPipe, bool kQ, bool kDerive>
 __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const GridDev& g,
                                                const double* __restrict__ tab,
                                                double* __restrict__ rec, const Ray& r,
@@ -199,7 +210,12 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   asm volatile("" ::: "memory");  // the record stores precede every record load
   const double T2 = fmax(r.T, kSegEps);
   double prev = r.amin;
-  LabMask lm = lab_mask(r.lab_min);  // label of the crossing at prev
+  // non-dominant axes (kDerive): masks h0 = [axis == A], h1 = [axis == B]
+  const int axA = r.D == 0 ? 1 : 0, axB = r.D == 2 ? 1 : 2;
+  auto derive_mask = [&](int lab) {
+    return LabMask{lab == axA ? kOneHi : 0, lab == axB ? kOneHi : 0, 0};
+  };
+  LabMask lm = kDerive ? derive_mask(r.lab_min) : lab_mask(r.lab_min);  // crossing at prev
   double pend = 0.0;
   // Ring of kLeanPipe in-flight segments (gather issued, value consumed
   // kLeanPipe steps later).  Steps run in blocks of kLeanPipe with the ring
@@ -212,7 +228,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   // it ends where slot j+1's segment starts), pick the winning crossing,
   // issue this segment's gather into slot j
   auto step = [&](int j) {
-    lean_consume<kMode, VT>(o, pend, st[j], st[(j + 1) % kLeanPipe].a);
+    lean_consume<kMode, kDerive, VT>(o, pend, st[j], st[(j + 1) % kLeanPipe].a);
     const bool c1 = an1 < an0;  // ties go to the lowest axis (_native.pyx:180-183)
     const double b01 = c1 ? an1 : an0;
     const bool c2 = an2 < b01;
@@ -256,7 +272,10 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     st[j].used = used;
     st[j].a = prev;
     st[j].m = lm;
-    lm = LabMask{m0 * kOneHi, m1 * kOneHi, m2 * kOneHi};
+    if constexpr (kDerive)
+      lm = derive_mask(static_cast<int>(k));
+    else
+      lm = LabMask{m0 * kOneHi, m1 * kOneHi, m2 * kOneHi};
     prev = cur;
   };
   const int n = r.count;
@@ -273,11 +292,11 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
 #pragma unroll
   for (int j = 0; j < kLeanPipe; ++j)
     if (j >= rem)
-      lean_consume<kMode, VT>(o, pend, st[j],
+      lean_consume<kMode, kDerive, VT>(o, pend, st[j],
                               j + 1 < kLeanPipe ? st[j + 1].a : (rem > 0 ? st[0].a : prev));
 #pragma unroll
   for (int j = 0; j + 1 < kLeanPipe; ++j)
-    if (j < rem) lean_consume<kMode, VT>(o, pend, st[j], j + 1 < rem ? st[j + 1].a : prev);
+    if (j < rem) lean_consume<kMode, kDerive, VT>(o, pend, st[j], j + 1 < rem ? st[j + 1].a : prev);
   // final segment [last crossing, amax]
   {
     const double cur = r.amax;
@@ -290,9 +309,25 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     last.v = __ldg(gp);
     last.used = used;
     last.m = lm;
-    lean_consume<kMode, VT>(o, pend, last, cur);
+    lean_consume<kMode, kDerive, VT>(o, pend, last, cur);
   }
-  lean_finish<kMode>(o, pend, r.lab_max, r.amax);
+  if constexpr (kMode == kLeanGrad) {
+    if constexpr (kDerive) {
+      lean_apply<true>(o, derive_mask(r.lab_max), r.amax, pend);
+      const double gc = r.lab_max == kConstLabel ? pend : 0.0;
+      const double hc = r.lab_max == kConstLabel ? pend * r.amax : 0.0;
+      const double gA = o.G0, gB = o.G1, hA = o.H0, hB = o.H1;
+      const double gD = -((gA + gB) + gc), hD = ((o.acc - hA) - hB) - hc;
+      o.G0 = r.D == 0 ? gD : gA;
+      o.H0 = r.D == 0 ? hD : hA;
+      o.G1 = r.D == 1 ? gD : (r.D == 0 ? gA : gB);
+      o.H1 = r.D == 1 ? hD : (r.D == 0 ? hA : hB);
+      o.G2 = r.D == 2 ? gD : gB;
+      o.H2 = r.D == 2 ? hD : hB;
+    } else {
+      lean_apply<false>(o, lab_mask(r.lab_max), r.amax, pend);
+    }
+  }
 }
 
 // Rays with a subnormal-scale direction component (Ray::safe: |d_a| <= 1e-20,
@@ -325,9 +360,12 @@ __device__ __forceinline__ void lean_walk(const VT* __restrict__ vol, const Grid
                                           const Ray& r, LeanSums& o) {
   if (r.safe)
     safe_walk<VT, kMode>(vol, g, tab, r, o);
+  else if (kMode == kLeanGrad && DRR_LEAN_DERIVE && r.lab_min != kConstLabel)
+    lean_walk_impl<VT, kMode, DRR_LEAN_PIPE_GRAD, DRR_LEAN_Q_GRAD, true>(vol, g, tab, rec, r, o);
   else
     lean_walk_impl<VT, kMode, kMode == kLeanGrad ? DRR_LEAN_PIPE_GRAD : DRR_LEAN_PIPE_FWD,
-                   kMode == kLeanGrad ? DRR_LEAN_Q_GRAD : DRR_LEAN_Q_FWD>(vol, g, tab, rec, r, o);
+                   kMode == kLeanGrad ? DRR_LEAN_Q_GRAD : DRR_LEAN_Q_FWD, false>(vol, g, tab, rec,
+                                                                                 r, o);
 }
 
 }  // namespace drr

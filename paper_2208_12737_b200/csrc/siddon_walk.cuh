@@ -137,6 +137,7 @@ struct Ray {
                     // belong to the next chunk (kNoEndLab for a ray's real exit)
   int flat;         // flat voxel index of the segment after amin
   int count;        // crossings this walk takes (the counted walk, siddon_lean.cuh)
+  int D;            // dominant axis: largest |d_a| / sp_a
   bool hit;
   bool safe;        // some |d_a| tiny: use IEEE '/' instead of the Markstein form
 };
@@ -266,6 +267,7 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
     if (w > wmax) { wmax = w; D = a; }
   }
   r.T = T;
+  r.D = D;
   // Start event per axis: (amin, entry) for chunk 0, else (alpha_D(b_j), D).
   double a_s = r.amin;
   int lab_s = -1;  // -1: entry semantics (every crossing with alpha >= amin)
