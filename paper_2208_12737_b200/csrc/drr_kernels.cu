@@ -29,16 +29,6 @@
 
 namespace drr {
 
-// Occupancy knob for experiments: DRR_MINB=n adds a minimum-blocks-per-SM
-// launch bound (0 = let ptxas choose).
-#ifndef DRR_MINB
-#define DRR_MINB 0
-#endif
-#if DRR_MINB > 0
-#define DRR_LB __launch_bounds__(kThreads, DRR_MINB)
-#else
-#define DRR_LB __launch_bounds__(kThreads)
-#endif
 // Launch bounds (A/B on C2, 32 poses, walk v6; scripts/gpu_ab.sh): the
 // gradient walks (k_forward_jac, k_backward) at 5 CTAs/SM with a 3-deep
 // gather pipeline and the forward at 6 CTAs/SM with a 4-deep one were the
@@ -128,57 +118,11 @@ __device__ __forceinline__ void store_out(OT* p, double v) {
   *p = static_cast<OT>(v);
 }
 
-// Endpoint gradients of one ray from the reverse-mode visitor
-// (see orc_raysum_endpoint_grad in oracle/siddon_oracle.c for the algebra).
-__device__ __forceinline__ void visitor_sums(const GradVisitor& v, double* G, double* Hh) {
-  G[0] = v.G0; G[1] = v.G1; G[2] = v.G2;
-  Hh[0] = v.H0; Hh[1] = v.H1; Hh[2] = v.H2;
-}
-__device__ __forceinline__ void visitor_sums(const GradVisitorSmem& v, double* G, double* Hh) {
-#pragma unroll
-  for (int a = 0; a < 3; ++a) { G[a] = v.G(a); Hh[a] = v.H(a); }
-}
-
-#if DRR_GRAD_SMEM
-using BwdVisitor = GradVisitorSmem;
-#else
-using BwdVisitor = GradVisitor;
-#endif
-
-__device__ __forceinline__ void visitor_init(GradVisitor&, double*) {}
-__device__ __forceinline__ void visitor_init(GradVisitorSmem& v, double* slots) { v.init(slots); }
-
-// Walk v5 (siddon_lean.cuh) by default; DRR_LEAN=0 builds the v4 visitor walk
-// for A/B.
-#ifndef DRR_LEAN
-#define DRR_LEAN 1
-#endif
-
+// The walk (siddon_lean.cuh) in its sum / count / gradient mode.
 template <typename VT, int kMode, bool kChunked>
 __device__ __forceinline__ void walk_sums(const VT* __restrict__ vol, const GridDev& g,
                                           double* tab, const Ray& r, LeanSums& o) {
-#if DRR_LEAN
   lean_walk<VT, kMode>(vol, g, tab, tab + plane_table_span(g), r, o);
-#else
-  if (kMode == kLeanSum) {
-    SumVisitor v;
-    walk<VT, kChunked>(vol, g, tab, tab + plane_table_span(g), r, v);
-    o.acc = v.acc;
-  } else if (kMode == kLeanCount) {
-    CountVisitor v;
-    walk<VT, kChunked>(vol, g, tab, tab + plane_table_span(g), r, v);
-    o.steps = v.steps;
-  } else {
-    BwdVisitor v;
-    visitor_init(v, tab + plane_table_span(g) + kWalkSmemDoublesPerThread * 128);
-    walk<VT, kChunked>(vol, g, tab, tab + plane_table_span(g), r, v);
-    double G[3], Hh[3];
-    visitor_sums(v, G, Hh);
-    o.acc = v.acc;
-    o.G0 = G[0]; o.G1 = G[1]; o.G2 = G[2];
-    o.H0 = Hh[0]; o.H1 = Hh[1]; o.H2 = Hh[2];
-  }
-#endif
 }
 
 // ---------------------------------------------------------------- forward
@@ -214,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FWD_MINB : DRR_SPLIT_MI
 }
 
 template <typename VT, int K>
-__global__ void DRR_LB
+__global__ void __launch_bounds__(kThreads)
     k_count(const VT* __restrict__ vol, const GridDev g,
             const double* __restrict__ frames, const DetDev det,
             int* __restrict__ steps) {
@@ -240,25 +184,6 @@ __global__ void DRR_LB
   }
   n = chunk_sum<K>(n);
   if (valid && chunk == 0) steps[(static_cast<size_t>(b) * det.H + h) * det.W + w] = n;
-}
-
-template <typename V>
-__device__ __forceinline__ void endpoint_grads(const Ray& r,
-                                               const V& v, double L,
-                                               double* dEds, double* dEdp) {
-  double G[3], Hh[3];
-  visitor_sums(v, G, Hh);
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    double gs = 0.0, gp = 0.0;
-    if (r.d[a] != 0.0) {
-      gs = L * (Hh[a] - G[a]) / r.d[a];
-      gp = -L * Hh[a] / r.d[a];
-    }
-    const double lt = r.d[a] / L * v.acc;
-    dEds[a] = gs - lt;
-    dEdp[a] = gp + lt;
-  }
 }
 
 // Endpoint gradients from summed walk totals (acc, G, H): the same algebra as
@@ -592,11 +517,7 @@ int check_launch(const char* what) {
 // Dynamic shared memory for the per-CTA plane table; >48 KB needs opt-in.
 size_t table_bytes(const drr::GridDev& g) {
   // plane table + the walk's per-thread constants (both kernels use <= 128 threads)
-#if DRR_LEAN
   const size_t per_thread = drr::kLeanRecDoublesPerThread;
-#else
-  const size_t per_thread = drr::kWalkSmemDoublesPerThread + drr::kGradSmemDoublesPerThread;
-#endif
   return (static_cast<size_t>(drr::plane_table_span(g)) + per_thread * 128) * sizeof(double);
 }
 

@@ -1,5 +1,8 @@
-// siddon_walk.cuh -- the per-ray incremental Siddon walk shared by every
-// kernel in drr_kernels.cu (forward, backward, step count, explicit rays).
+// siddon_walk.cuh -- grid / ray types, the per-ray setup (slab entry and
+// exit, first crossings, crossing count, fast-voxel certificate, ray
+// splitting) and the select-based walk (v4) with its visitors.  The kernels
+// walk with siddon_lean.cuh; the v4 walk here serves rays whose direction has
+// a subnormal-scale component (Ray::safe), which need IEEE division.
 //
 // Semantics are those of the reference's vectorised Siddon kernel
 // (_native.pyx:140-193 / python_ref.py:130-138): the ray R(a) = s + a (p - s),
@@ -334,9 +337,8 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
   r.flat = vox[0] + g.stride[1] * vox[1] + g.stride[2] * vox[2];
 }
 
-// Gather pipeline depth: segment i's voxel load is consumed in iteration
-// i + kPipe, so up to kPipe gathers per ray are in flight (ncu: the gather's
-// long-scoreboard stall dominated at depth 1).
+// Gather pipeline depth of the v4 walk (segment i's voxel load is consumed in
+// iteration i + DRR_PIPE).
 #ifndef DRR_PIPE
 #define DRR_PIPE 1
 #endif
@@ -418,17 +420,6 @@ __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
   vis.finish(r.lab_max, amax);
 }
 
-// Per-thread shared-memory doubles the walk needs beyond the plane table
-// (the smem-constant variant that used them lost the A/B, see profiles/).
-constexpr int kWalkSmemDoublesPerThread = 0;
-
-template <typename VT, bool kChunked = false, typename Visitor>
-__device__ __forceinline__ void walk(const VT* __restrict__ vol, const GridDev& g,
-                                     const double* __restrict__ tab, double* /*cst*/,
-                                     const Ray& r, Visitor& vis) {
-  walk_select<VT, kChunked>(vol, g, tab, r, vis);
-}
-
 // ---- visitors ----------------------------------------------------------
 
 struct SumVisitor {
@@ -482,45 +473,5 @@ struct GradVisitor {
     apply(lab_end, a_end, pend);
   }
 };
-
-// Same reverse-mode visitor with the six per-axis accumulators parked in
-// shared memory, indexed by the crossing's label: one LDS/STS pair per
-// accumulator instead of three compares + six selects, and 12 fewer live
-// registers.  Layout is [slot][thread] (conflict-free for any label mix);
-// slot 3 absorbs clip labels (no tangent).
-struct GradVisitorSmem {
-  double acc = 0.0;
-  double pend = 0.0;
-  double* base;  // this thread's slot 0; slot k at base[k * nt]
-  int nt;
-  __device__ __forceinline__ void init(double* cta_slots) {
-    nt = blockDim.x;
-    base = cta_slots + threadIdx.x;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) base[k * nt] = 0.0;
-  }
-  __device__ __forceinline__ void apply(int label, double alpha, double c) {
-    double* p = base + 2 * label * nt;
-    p[0] = p[0] + c;
-    p[nt] = __fma_rn(c, alpha, p[nt]);
-  }
-  __device__ __forceinline__ void segment(bool used, double seg, double v,
-                                          int lab_start, double a_start) {
-    const double vv = used ? v : 0.0;
-    acc = acc + seg * vv;
-    apply(lab_start, a_start, pend - vv);
-    pend = vv;
-  }
-  __device__ __forceinline__ void finish(int lab_end, double a_end) {
-    apply(lab_end, a_end, pend);
-  }
-  __device__ __forceinline__ double G(int a) const { return base[2 * a * nt]; }
-  __device__ __forceinline__ double H(int a) const { return base[(2 * a + 1) * nt]; }
-};
-
-#ifndef DRR_GRAD_SMEM
-#define DRR_GRAD_SMEM 1
-#endif
-constexpr int kGradSmemDoublesPerThread = DRR_GRAD_SMEM ? 8 : 0;
 
 }  // namespace drr
