@@ -107,6 +107,17 @@ class Detector:
                                     self.ray_split)
 
 
+# One launch covers at most this many poses (the grid's z extent); larger
+# batches are split into launches of this size (rays are independent, so the
+# split does not change any result).
+MAX_POSES_PER_LAUNCH = 65535
+
+
+def _pose_chunks(B: int):
+    for lo in range(0, B, MAX_POSES_PER_LAUNCH):
+        yield lo, min(B, lo + MAX_POSES_PER_LAUNCH)
+
+
 def render_frames(vol: DeviceVolume, det: Detector, frames: torch.Tensor,
                   out_dtype=torch.float32) -> torch.Tensor:
     """(B, 12) float64 frames -> (B, H, W) images via ``drr_forward``."""
@@ -115,9 +126,11 @@ def render_frames(vol: DeviceVolume, det: Detector, frames: torch.Tensor,
     B = frames.shape[0]
     img = torch.empty((B, det.height, det.width), dtype=out_dtype, device=frames.device)
     lib = _lib.load()
-    _lib.check(lib.drr_forward(vol.flat.data_ptr(), vol.vol_dtype, vol.grid, frames.data_ptr(),
-                               B, det.c, img.data_ptr(), 1 if out_dtype == torch.float64 else 0,
-                               _stream_ptr(frames.device)))
+    for lo, hi in _pose_chunks(B):
+        _lib.check(lib.drr_forward(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
+                                   frames[lo:hi].data_ptr(), hi - lo, det.c, img[lo:hi].data_ptr(),
+                                   1 if out_dtype == torch.float64 else 0,
+                                   _stream_ptr(frames.device)))
     return img
 
 
@@ -130,17 +143,18 @@ def backward_frames(vol: DeviceVolume, det: Detector, frames: torch.Tensor,
     grad_img = grad_img.contiguous()
     B = frames.shape[0]
     lib = _lib.load()
-    ws_bytes = lib.drr_backward_workspace_size(B, det.c)
+    ws_bytes = lib.drr_backward_workspace_size(min(B, MAX_POSES_PER_LAUNCH), det.c)
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=frames.device)
     grad_frames = torch.empty((B, 12), dtype=torch.float64, device=frames.device)
     img = None
     if want_image:
         img = torch.empty((B, det.height, det.width), dtype=torch.float32, device=frames.device)
-    _lib.check(lib.drr_backward(
-        vol.flat.data_ptr(), vol.vol_dtype, vol.grid, frames.data_ptr(), B, det.c,
-        grad_img.data_ptr(), 1 if grad_img.dtype == torch.float64 else 0,
-        grad_frames.data_ptr(), img.data_ptr() if img is not None else None, 0,
-        ws.data_ptr(), ws_bytes, _stream_ptr(frames.device)))
+    for lo, hi in _pose_chunks(B):
+        _lib.check(lib.drr_backward(
+            vol.flat.data_ptr(), vol.vol_dtype, vol.grid, frames[lo:hi].data_ptr(), hi - lo, det.c,
+            grad_img[lo:hi].data_ptr(), 1 if grad_img.dtype == torch.float64 else 0,
+            grad_frames[lo:hi].data_ptr(), img[lo:hi].data_ptr() if img is not None else None, 0,
+            ws.data_ptr(), ws_bytes, _stream_ptr(frames.device)))
     return (grad_frames, img) if want_image else grad_frames
 
 
@@ -152,7 +166,8 @@ def jac_bytes(det: Detector, n_poses: int) -> int:
 def render_frames_jac(vol: DeviceVolume, det: Detector, frames: torch.Tensor,
                       out_dtype=torch.float32):
     """Image (B, H, W) plus the per-ray Jacobian (6, B*H*W) float64 from ONE
-    walk (``drr_forward_jac``); :func:`backward_from_jac` turns it into dL/dframe."""
+    walk (``drr_forward_jac``); :func:`backward_from_jac` turns it into dL/dframe.
+    One launch: B <= MAX_POSES_PER_LAUNCH."""
     _require_cuda(frames, "frames")
     frames = frames.detach().to(torch.float64).contiguous()
     B = frames.shape[0]
@@ -189,9 +204,10 @@ def count_steps(vol: DeviceVolume, det: Detector, frames: torch.Tensor) -> torch
     B = frames.shape[0]
     steps = torch.empty((B, det.height, det.width), dtype=torch.int32, device=frames.device)
     lib = _lib.load()
-    _lib.check(lib.drr_count_steps(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
-                                   frames.data_ptr(), B, det.c, steps.data_ptr(),
-                                   _stream_ptr(frames.device)))
+    for lo, hi in _pose_chunks(B):
+        _lib.check(lib.drr_count_steps(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
+                                       frames[lo:hi].data_ptr(), hi - lo, det.c,
+                                       steps[lo:hi].data_ptr(), _stream_ptr(frames.device)))
     return steps
 
 
@@ -205,13 +221,14 @@ class _RenderFrames(torch.autograd.Function):
 
     When a gradient is needed, forward is ``drr_forward_jac`` (one walk: image
     plus per-ray Jacobian) and backward the walk-free ``drr_backward_jac``;
-    above ``JAC_BUDGET_BYTES`` forward is ``drr_forward`` and backward the
-    fused re-walk ``drr_backward``."""
+    above ``JAC_BUDGET_BYTES`` (or one launch's pose limit) forward is
+    ``drr_forward`` and backward the fused re-walk ``drr_backward``."""
 
     @staticmethod
     def forward(ctx, frames, vol, det):
         ctx.vol, ctx.det = vol, det
-        if ctx.needs_input_grad[0] and jac_bytes(det, frames.shape[0]) <= JAC_BUDGET_BYTES:
+        if (ctx.needs_input_grad[0] and frames.shape[0] <= MAX_POSES_PER_LAUNCH
+                and jac_bytes(det, frames.shape[0]) <= JAC_BUDGET_BYTES):
             img, jac = render_frames_jac(vol, det, frames)
             ctx.save_for_backward(frames, jac)
             return img

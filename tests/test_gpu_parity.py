@@ -421,3 +421,22 @@ def test_module_uses_one_walk_and_rewalk_fallback(golden, cuda_device, monkeypat
     monkeypatch.setattr(renderer, "JAC_BUDGET_BYTES", 0)
     rewalk = grad()
     np.testing.assert_allclose(one_walk, rewalk, rtol=1e-12, atol=1e-15)
+
+
+def test_pose_batches_beyond_one_launch(golden, cuda_device, monkeypatch):
+    """Batches larger than one launch's pose limit are split into launches;
+    rays are independent, so images, step counts and gradients are unchanged."""
+    from paper_2208_12737_b200 import (Detector, backward_frames, count_steps, render_frames,
+                                       renderer)
+    vol = _vol_from_golden(golden, "ps_")
+    det = Detector(21, 21, 4.0, ray_split=1)
+    frames = torch.tensor(np.stack([O.pose_frame(e, golden["ps_center"]) for e in golden["ps_poses"]]),
+                          device=cuda_device)
+    g = torch.randn((frames.shape[0], 21, 21), device=cuda_device, dtype=torch.float64)
+    whole = (render_frames(vol, det, frames), count_steps(vol, det, frames),
+             backward_frames(vol, det, frames, g))
+    monkeypatch.setattr(renderer, "MAX_POSES_PER_LAUNCH", 2)
+    split = (render_frames(vol, det, frames), count_steps(vol, det, frames),
+             backward_frames(vol, det, frames, g))
+    for a, b in zip(whole, split):
+        assert torch.equal(a, b)
