@@ -440,3 +440,33 @@ def test_pose_batches_beyond_one_launch(golden, cuda_device, monkeypatch):
              backward_frames(vol, det, frames, g))
     for a, b in zip(whole, split):
         assert torch.equal(a, b)
+
+
+def test_clip_entry_and_exit_gradients(cuda_device):
+    """Rays that start inside the volume (clip entry: the 3-axis gradient
+    walk) and rays that end inside it (clip exit: the derived-axis walk with
+    its clip terms), energies bitwise and endpoint gradients to 1e-10 against
+    the C oracle."""
+    be = _backend()
+    rng = np.random.default_rng(23)
+    for trial in range(24):
+        dims = tuple(int(x) for x in rng.integers(2, 20, 3))
+        spacing = rng.uniform(0.5, 2.5, 3)
+        origin = rng.uniform(-3, 3, 3)
+        flat = rng.uniform(0, 4, int(np.prod(dims)))
+        lo = origin
+        hi = origin + np.asarray(dims) * spacing
+        span = float(max(hi - lo))
+        if trial % 2:
+            src = rng.uniform(lo, hi)                       # source inside
+            pix = rng.uniform(lo - span, hi + span, size=(128, 3))
+        else:
+            src = rng.uniform(lo - 3 * span, hi + 3 * span)  # pixel inside
+            pix = rng.uniform(lo, hi, size=(128, 3))
+        e = be.siddon_raysum(flat, dims, spacing, origin, src, pix)
+        np.testing.assert_array_equal(e, O.raysum(flat, dims, spacing, origin, src, pix))
+        _, gs, gp = be.ray_endpoint_grad(flat, dims, spacing, origin, src, pix)
+        _, rs, rp = O.raysum_endpoint_grad(flat, dims, spacing, origin, src, pix)
+        sc = max(1.0, np.abs(rs).max(), np.abs(rp).max())
+        np.testing.assert_allclose(gs, rs, atol=1e-10 * sc, rtol=0, err_msg=f"trial {trial}")
+        np.testing.assert_allclose(gp, rp, atol=1e-10 * sc, rtol=0, err_msg=f"trial {trial}")
