@@ -1,19 +1,24 @@
 // drr_kernels.cu -- sm_100a kernels and the extern "C" ABI of include/drr_b200.h.
 //
-// Kernels (all gather-bound; no dense contraction, so no tensor cores):
-//   k_forward      one thread per detector pixel of a B x H x W batch; the
-//                  pixel ray is generated in-kernel from the pose frame
-//                  (geometry.py:152-175 fused with _native.pyx:140-193);
-//                  CTAs cover 16 x 8 pixel tiles whose warps are 8 x 4
-//                  quads, so neighbouring rays gather neighbouring voxels.
-//   k_backward     the fused re-walk: per pixel dE/ds, dE/dp (reverse mode),
-//                  weighted by the upstream pixel gradient and reduced per
-//                  CTA to the 12 frame gradients in a fixed order.
+// Every kernel generates its pixel rays in-kernel from the pose frame
+// (geometry.py:152-175) and walks them with siddon_lean.cuh (the reference's
+// _native.pyx:140-282 semantics, bit-identical crossing parameters).  No dense
+// contraction anywhere, so no tensor cores.  CTAs cover pixel tiles whose warps
+// are 8 x 4 quads, so neighbouring rays gather neighbouring voxels.
+//   k_forward        image of a B x H x W batch
+//   k_forward_jac    image + each ray's endpoint Jacobian dE/ds, dE/dp (one
+//                    walk per ray for the whole fwd+bwd step)
+//   k_backward_jac   contraction of the stored Jacobians with the pixel
+//                    gradient, per-CTA partials of the 12 frame gradients
+//   k_backward       the same gradient by re-walking the rays (Jacobian-budget
+//                    fallback)
 //   k_reduce_frames  fixed-order second pass over the CTA partials (no atomics
-//                  anywhere, so gradients are bit-reproducible: SPEC.md:289).
-//   k_raysum / k_raysum_grad   explicit-ray forms for the kernel-protocol
-//                  backend (the reference's _kernels plugin boundary).
-//   k_count        used voxel-steps per ray (roofline denominator).
+//                    anywhere, so gradients are bit-reproducible: SPEC.md:289)
+//   k_raysum / k_raysum_grad  explicit-ray forms for the kernel-protocol
+//                    backend (the reference's _kernels plugin boundary)
+//   k_count          used voxel-steps per ray (roofline denominator)
+// loss_kernels.cuh / pose_kernels.cuh hold the loss, pose-frame and
+// registration-update kernels of the batched loss_and_gradient chain.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -29,10 +34,11 @@
 
 namespace drr {
 
-// Launch bounds (A/B on C2, 32 poses, walk v6; scripts/gpu_ab.sh): the
+// Launch bounds (A/B on C2, 32 poses; scripts/gpu_ab.sh, gpu_ab_fast.sh): the
 // gradient walks (k_forward_jac, k_backward) at 5 CTAs/SM with a 3-deep
 // gather pipeline and the forward at 6 CTAs/SM with a 4-deep one were the
-// fastest of the spill-free combinations (2.64 ms / 2.0 ms for 32 poses).
+// fastest combinations (2.56 ms / 2.08 ms for 32 poses); ptxas spills only
+// outside the walk's fast path.
 #ifndef DRR_BWD_MINB
 #define DRR_BWD_MINB 5
 #endif
@@ -118,7 +124,8 @@ __device__ __forceinline__ void store_out(OT* p, double v) {
   *p = static_cast<OT>(v);
 }
 
-// The walk (siddon_lean.cuh) in its sum / count / gradient mode.
+// The walk (siddon_lean.cuh) in its sum / count / gradient mode; chunked walks
+// (K > 1) are described by the Ray itself (ray_setup).
 template <typename VT, int kMode, bool kChunked>
 __device__ __forceinline__ void walk_sums(const VT* __restrict__ vol, const GridDev& g,
                                           double* tab, const Ray& r, LeanSums& o) {
