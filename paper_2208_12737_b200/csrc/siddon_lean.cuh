@@ -141,6 +141,30 @@ __device__ __forceinline__ void lds_2f64(uint32_t addr, double& a, double& b) {
 // predicate on the load).
 __device__ const double g_zero_voxel = 0.0;
 
+// The voxel gather: read-only path; DRR_GATHER_HINT selects a cache-policy
+// qualifier (0 = plain ld.global.nc).  A/B on C2 (scripts/gpu_ab_fast.sh):
+// the 256-byte L2 prefetch hint (5) is ~1% faster than plain; L1 evict-first
+// or no-allocate lose 8-19%; evict-last and 128-byte prefetch are neutral.
+#ifndef DRR_GATHER_HINT
+#define DRR_GATHER_HINT 5
+#endif
+__device__ __forceinline__ float gather_voxel(const float* p) {
+#if DRR_GATHER_HINT == 1
+  float v; asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(p)); return v;
+#elif DRR_GATHER_HINT == 2
+  float v; asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p)); return v;
+#elif DRR_GATHER_HINT == 3
+  float v; asm volatile("ld.global.nc.L2::128B.f32 %0, [%1];" : "=f"(v) : "l"(p)); return v;
+#elif DRR_GATHER_HINT == 4
+  float v; asm volatile("ld.global.nc.L1::evict_first.f32 %0, [%1];" : "=f"(v) : "l"(p)); return v;
+#elif DRR_GATHER_HINT == 5
+  float v; asm volatile("ld.global.nc.L2::256B.f32 %0, [%1];" : "=f"(v) : "l"(p)); return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double gather_voxel(const double* p) { return __ldg(p); }
+
 // Exact path (out of the fast path): the used test and the reference's
 // floored midpoint (_native.pyx:68-82, 186), with s and d from the record.
 // Returns the address to gather (the zero voxel for a skipped segment).
@@ -268,7 +292,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     const double seg = cur - prev;
     if (!(seg > T2)) gp = lean_exact(vol, g, sd_s, sd_stride, prev, cur, seg, used);
     bp += db;
-    st[j].v = __ldg(gp);
+    st[j].v = gather_voxel(gp);
     st[j].used = used;
     st[j].a = prev;
     st[j].m = lm;
@@ -306,7 +330,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     if (!(seg > T2)) gp = lean_exact(vol, g, sd_s, sd_stride, prev, cur, seg, used);
     LeanStage<VT> last;
     last.a = prev;
-    last.v = __ldg(gp);
+    last.v = gather_voxel(gp);
     last.used = used;
     last.m = lm;
     lean_consume<kMode, kDerive, VT>(o, pend, last, cur);
