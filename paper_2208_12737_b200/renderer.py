@@ -16,8 +16,9 @@ equivalent of the reference's ``render`` / ``render_with_gradient`` /
 
 With a gradient requested, the image and every ray's endpoint Jacobian come
 from one walk (``drr_forward_jac``) and backward is a walk-free contraction
-(``drr_backward_jac``); without one, ``drr_forward`` alone runs.  torch autograd
-only chains the 12 frame numbers to the pose (``geometry.pose_frames``).
+(``drr_backward_jac``); without one, ``drr_forward`` alone runs.  The pose ->
+frame map and its gradient are ``drr_pose_frames`` / ``drr_pose_grad``
+(``geometry.pose_frames`` is the same map as torch ops, used on the host side).
 """
 
 from __future__ import annotations
@@ -246,6 +247,37 @@ class _RenderFrames(torch.autograd.Function):
         return grad_frames.to(frames.dtype), None, None
 
 
+class _PoseFrames(torch.autograd.Function):
+    """(B, 7) pose vectors -> (B, 12) frames with ``drr_pose_frames``; backward
+    is ``drr_pose_grad`` (dL/dframe -> dL/deta).  Two launches instead of the
+    ~60 small torch ops of ``geometry.pose_frames``, the same map
+    (``geometry.py:120-149``)."""
+
+    @staticmethod
+    def forward(ctx, eta, isocenter):
+        import ctypes
+        eta = eta.detach().to(torch.float64).contiguous()
+        B = eta.shape[0]
+        frames = torch.empty((B, 12), dtype=torch.float64, device=eta.device)
+        iso = (ctypes.c_double * 3)(*isocenter)
+        lib = _lib.load()
+        _lib.check(lib.drr_pose_frames(eta.data_ptr(), B, iso, frames.data_ptr(),
+                                       _stream_ptr(eta.device)))
+        ctx.save_for_backward(eta)
+        return frames
+
+    @staticmethod
+    def backward(ctx, grad_frames):
+        (eta,) = ctx.saved_tensors
+        B = eta.shape[0]
+        grad_frames = grad_frames.to(torch.float64).contiguous()
+        grad_eta = torch.empty((B, 7), dtype=torch.float64, device=eta.device)
+        lib = _lib.load()
+        _lib.check(lib.drr_pose_grad(eta.data_ptr(), grad_frames.data_ptr(), B,
+                                     grad_eta.data_ptr(), _stream_ptr(eta.device)))
+        return grad_eta, None
+
+
 def render_pose_vectors(vol: DeviceVolume, det: Detector, eta: torch.Tensor,
                         isocenter=None) -> torch.Tensor:
     """Differentiable render of (B, 7) pose vectors (rho, theta, phi, gamma, shift)."""
@@ -316,6 +348,6 @@ class DRR(torch.nn.Module):
             check_pose_vectors(eta.detach())
             if torch.is_grad_enabled() and eta.requires_grad:
                 check_gimbal(eta.detach())
-        frames = pose_frames(eta, self.isocenter)
+        frames = _PoseFrames.apply(eta, self.isocenter)
         img = _RenderFrames.apply(frames, self.volume, self.detector)
         return img[0] if single else img
