@@ -144,3 +144,30 @@ def test_registration_failure_modes(cuda_device):
     assert tr.failed and not tr.converged and len(tr.losses) == 1 and np.isinf(tr.losses[0])
     tr = register(fixed, vol, (100.0, 0.3, 0.0, 0.0, 0.0, 0.0, 0.0), det, OptimizerConfig(max_iters=5))
     assert tr.failed
+
+
+def test_module_losses_fused_match_torch(cuda_device):
+    """metrics.neg_zncc / l2 on float32 device images run the fused loss kernel
+    (value + the reference's analytic pixel gradient); they match the plain
+    torch restatement (values to 1e-12, pixel gradients to 1e-6 relative --
+    fp32 stored gradient) for batched, single, shared and per-image fixed."""
+    from paper_2208_12737_b200 import metrics
+    rng = np.random.default_rng(4)
+    a = torch.tensor(rng.random((3, 17, 13)) * 50, device=cuda_device, dtype=torch.float32)
+    fixed_shared = torch.tensor(rng.random((17, 13)) * 50, device=cuda_device, dtype=torch.float32)
+    fixed_each = torch.tensor(rng.random((3, 17, 13)) * 50, device=cuda_device, dtype=torch.float32)
+    for name in ("neg_zncc", "l2"):
+        fn = getattr(metrics, name)
+        for moving, fixed in ((a, fixed_shared), (a, fixed_each), (a[1], fixed_shared),
+                              (a[1], fixed_each[1])):
+            x = moving.clone().requires_grad_(True)
+            v = fn(x, fixed)
+            v.sum().backward()
+            # the torch restatement (float64 path)
+            y = moving.double().clone().requires_grad_(True)
+            w = fn(y, fixed.double())
+            w.sum().backward()
+            np.testing.assert_allclose(v.detach().cpu().numpy(), w.detach().cpu().numpy(),
+                                       rtol=1e-12, atol=1e-12)
+            gx, gy = x.grad.double().cpu().numpy(), y.grad.cpu().numpy()
+            np.testing.assert_allclose(gx, gy, rtol=1e-6, atol=1e-6 * np.abs(gy).max())
