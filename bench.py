@@ -265,10 +265,16 @@ def main():
     from paper_2208_12737_b200 import _lib
     from paper_2208_12737_b200.metrics import neg_zncc
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # DRR_BENCH_SHARED_GPU=1 (testing only) puts every rank on cuda:0 with the
+    # gloo backend, so the multi-rank path can be exercised on a one-GPU box.
+    shared = os.environ.get("DRR_BENCH_SHARED_GPU") == "1"
+    dev = torch.device("cuda", 0 if shared else local)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     # --- volume: built on rank 0, NCCL-broadcast once --------
     if rank == 0:
@@ -338,7 +344,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev.index) as clk:
         times = timed(lambda: step(eta0), args.steps, 0)
     torch.cuda.synchronize(dev)
     if world > 1:
