@@ -2,8 +2,10 @@
 
 Drop-in for the hot path of arXiv 2208.12737 (DiffDRR) as restated by the
 reference package ``drrtrace``: ``DRR(volume, spacing, sdr, height, delx)``
-(north-star module API) and the ``"cuda"`` kernel-protocol backend (the
-reference's ``_kernels.get_backend`` plugin boundary).  All compute runs in
+(north-star module API), ``api`` (drrtrace's functional API: render,
+render_with_gradient, loss_and_gradient, register, with its types) and the
+``"cuda"`` kernel-protocol backend (the reference's ``_kernels.get_backend``
+plugin boundary).  All compute runs in
 hand-written sm_100a CUDA behind the C ABI of ``include/drr_b200.h``.
 """
 

@@ -50,7 +50,8 @@ class DeviceVolume:
         if isinstance(data, torch.Tensor):
             t = data.detach()
         else:
-            t = torch.as_tensor(np.asarray(data))
+            arr = np.asarray(data)
+            t = torch.as_tensor(arr if arr.flags.writeable else arr.copy())
         if t.ndim != 3:
             raise InvalidArgumentError(f"volume must be 3-D (nx, ny, nz), got shape {tuple(t.shape)}")
         if any(n < 1 for n in t.shape):
