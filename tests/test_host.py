@@ -130,3 +130,39 @@ def test_gimbal_guard_host():
         check_pose_vectors(torch.tensor([[-1.0, 0.3, 1.0, 0, 0, 0, 0]]))
     with pytest.raises(InvalidArgumentError):
         check_pose_vectors(torch.tensor([[1.0, float("nan"), 1.0, 0, 0, 0, 0]]))
+
+
+def test_api_types_mirror_reference():
+    """api.Volume / PoseParameters / DetectorSpec / Image validate like the
+    reference's dataclasses (volume.py:24-83, geometry.py:32-97,
+    raytrace.py:29-47) and carry the same values; reference objects are
+    accepted where ours are (same field names)."""
+    import numpy as np
+    import pytest
+    from paper_2208_12737_b200 import api
+    from paper_2208_12737_b200.errors import InvalidArgumentError
+    bad = [lambda m: m.PoseParameters(0.0, 0.1, 1.0),
+           lambda m: m.PoseParameters(100.0, float("nan"), 1.0),
+           lambda m: m.DetectorSpec(0, 3),
+           lambda m: m.DetectorSpec(3, 3, (0.0, 1.0)),
+           lambda m: m.Volume((2, 2, 2), (1, -1, 1), (0, 0, 0), np.zeros(8)),
+           lambda m: m.Volume((2, 2, 2), (1, 1, 1), (0, 0, 0), np.zeros(7)),
+           lambda m: m.Image(np.zeros(3))]
+    for make in bad:
+        with pytest.raises(InvalidArgumentError):
+            make(api)
+    v = api.Volume((3, 4, 5), (1.0, 2.0, 0.5), (1.0, -2.0, 0.0), np.arange(60.0))
+    p = api.PoseParameters.from_vector([300.0, 0.4, 1.3, 0.1, 1.0, 2.0, 3.0])
+    s = api.DetectorSpec.for_volume(v, 7, 9, 2.5)
+    dt = O.reference_module()
+    if dt is None:
+        return
+    for make in bad:
+        with pytest.raises(dt.errors.InvalidArgumentError if hasattr(dt, "errors") else Exception):
+            make(dt)
+    rv = dt.Volume((3, 4, 5), (1.0, 2.0, 0.5), (1.0, -2.0, 0.0), np.arange(60.0))
+    assert v.center == rv.center and np.array_equal(v.flat_data(), rv.flat_data())
+    assert np.array_equal(p.to_vector(), dt.PoseParameters.from_vector(p.to_vector()).to_vector())
+    rs = dt.DetectorSpec.for_volume(rv, 7, 9, 2.5)
+    assert (s.height, s.width, s.pixel_pitch, s.isocenter) == \
+        (rs.height, rs.width, rs.pixel_pitch, rs.isocenter)
