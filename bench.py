@@ -469,7 +469,7 @@ def main():
                 "h2d_bytes_per_step": int(h_eta.numel() * 8),
                 "d2h_bytes_per_step": int(h_out.numel() * 8)},
         "gpu_launches": 6 * args.steps,
-        "module_path": {"api": "DRR nn.Module + torch neg_zncc + autograd",
+        "module_path": {"api": "DRR nn.Module + metrics.neg_zncc + torch autograd",
                         "ms_per_step": module_ms, "value": B / (module_ms / 1e3)},
         "roofline": {"bound": "hbm",
                      "kernel": "k_forward_jac (the one CT walk per step: image + ray Jacobian)",
