@@ -521,10 +521,12 @@ int check_launch(const char* what) {
   return DRR_OK;
 }
 
-// Dynamic shared memory for the per-CTA plane table; >48 KB needs opt-in.
-size_t table_bytes(const drr::GridDev& g) {
-  // plane table + the walk's per-thread constants (both kernels use <= 128 threads)
-  const size_t per_thread = drr::kLeanRecDoublesPerThread;
+// Dynamic shared memory: the per-CTA plane table plus the walk's per-thread
+// ray records (every walk kernel has 128 threads).  Only what the walk mode
+// uses is allocated -- shared memory comes out of the same 228 KB per SM as
+// the L1 cache that serves the CT gathers.  >48 KB needs opt-in.
+size_t table_bytes(const drr::GridDev& g, bool grad_walk) {
+  const size_t per_thread = drr::lean_rec_doubles(grad_walk);
   return (static_cast<size_t>(drr::plane_table_span(g)) + per_thread * 128) * sizeof(double);
 }
 
@@ -565,9 +567,9 @@ int make_grid(const drr_grid* in, drr::GridDev& g) {
   g.stride[1] = g.n[0];
   g.stride[2] = g.n[0] * g.n[1];
   g.total = static_cast<int>(total);
-  if (table_bytes(g) > 227 * 1024)
+  if (table_bytes(g, true) > 227 * 1024)
     return fail(DRR_ERR_INVALID_ARGUMENT, "plane table of %zu bytes exceeds shared memory",
-                table_bytes(g));
+                table_bytes(g, true));
   return DRR_OK;
 }
 
@@ -628,7 +630,7 @@ void launch_backward(const VT* vol, const drr::GridDev& g,
                             const double* frames, const drr::DetDev& d,
                             int n_poses, const GT* grad, void* img,
                             int img_dtype, double* partials, cudaStream_t st) {
-  const size_t smem = table_bytes(g);
+  const size_t smem = table_bytes(g, true);
   const int K = ray_split(d, n_poses);
   const dim3 grd = pose_grid(d, n_poses, K);
   DRR_DISPATCH_K(K,
@@ -657,7 +659,7 @@ int drr_raysum(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::GridDev g;
   int rc = make_grid(grid, g);
   if (rc) return rc;
-  const size_t smem = table_bytes(g);
+  const size_t smem = table_bytes(g, false);
   if (n_rays < 0) return fail(DRR_ERR_INVALID_ARGUMENT, "n_rays < 0");
   if (n_rays == 0) return DRR_OK;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -685,7 +687,7 @@ int drr_raysum_endpoint_grad(const void* d_vol, int vol_dtype,
   drr::GridDev g;
   int rc = make_grid(grid, g);
   if (rc) return rc;
-  const size_t smem = table_bytes(g);
+  const size_t smem = table_bytes(g, true);
   if (n_rays < 0) return fail(DRR_ERR_INVALID_ARGUMENT, "n_rays < 0");
   if (n_rays == 0) return DRR_OK;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -713,7 +715,7 @@ int drr_forward(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::DetDev d;
   int rc = make_grid(grid, g);
   if (rc) return rc;
-  const size_t smem = table_bytes(g);
+  const size_t smem = table_bytes(g, false);
   rc = make_det(det, d);
   if (rc) return rc;
   if (n_poses < 0 || n_poses > 65535)
@@ -763,7 +765,7 @@ int drr_forward_jac(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::DetDev d;
   int rc = make_grid(grid, g);
   if (rc) return rc;
-  const size_t smem = table_bytes(g);
+  const size_t smem = table_bytes(g, true);
   rc = make_det(det, d);
   if (rc) return rc;
   if (n_poses < 0 || n_poses > 65535)
@@ -839,7 +841,7 @@ int drr_backward(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::DetDev d;
   int rc = make_grid(grid, g);
   if (rc) return rc;
-  const size_t smem = table_bytes(g);
+  const size_t smem = table_bytes(g, true);
   rc = make_det(det, d);
   if (rc) return rc;
   if (n_poses < 0 || n_poses > 65535)
@@ -882,7 +884,7 @@ int drr_count_steps(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::DetDev d;
   int rc = make_grid(grid, g);
   if (rc) return rc;
-  const size_t smem = table_bytes(g);
+  const size_t smem = table_bytes(g, false);
   rc = make_det(det, d);
   if (rc) return rc;
   if (n_poses < 0 || n_poses > 65535)

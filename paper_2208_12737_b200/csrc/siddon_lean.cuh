@@ -47,7 +47,12 @@ namespace drr {
 #ifndef DRR_LEAN_Q_GRAD
 #define DRR_LEAN_Q_GRAD 1
 #endif
-constexpr int kLeanRecDoublesPerThread = 14;
+constexpr int kLeanRecDoublesPerThread = 14;  // the largest record (kQ)
+// Record doubles per thread a walk mode uses: {s, d} x 3 and 1/d x 3, plus
+// (kQ) the steps next to 1/d and the 3 table cursors.
+__host__ __device__ constexpr int lean_rec_doubles(bool grad_walk) {
+  return (grad_walk ? DRR_LEAN_Q_GRAD : DRR_LEAN_Q_FWD) ? 14 : 9;
+}
 constexpr int kLeanThreads = 128;  // threads per CTA of every kernel using the walk
 
 enum LeanMode { kLeanSum = 0, kLeanCount = 1, kLeanGrad = 2 };
