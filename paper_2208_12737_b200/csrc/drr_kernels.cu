@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FWD_MINB : DRR_SPLIT_MI
               const double* __restrict__ frames, const DetDev det,
               OT* __restrict__ img) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, tab);
+  build_plane_table(g, frames + 12 * blockIdx.z, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
   tile_ray<K>(h, w, chunk);
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads)
             const double* __restrict__ frames, const DetDev det,
             int* __restrict__ steps) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, tab);
+  build_plane_table(g, frames + 12 * blockIdx.z, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
   tile_ray<K>(h, w, chunk);
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
                const GT* __restrict__ grad_img, OT* __restrict__ img,
                double* __restrict__ partials) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, tab);
+  build_plane_table(g, frames + 12 * blockIdx.z, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
   tile_ray<K>(h, w, chunk);
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
                   const double* __restrict__ frames, const DetDev det,
                   OT* __restrict__ img, double* __restrict__ jac, size_t npix_total) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, tab);
+  build_plane_table(g, frames + 12 * blockIdx.z, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
   tile_ray<K>(h, w, chunk);
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kRayThreads)
              const double* __restrict__ src, const double* __restrict__ pix,
              int64_t n_rays, double* __restrict__ out) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, tab);
+  build_plane_table(g, src, tab);
   __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_rays) return;
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kRayThreads)
                   double* __restrict__ out, double* __restrict__ dEds,
                   double* __restrict__ dEdp) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, tab);
+  build_plane_table(g, src, tab);
   __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_rays) return;

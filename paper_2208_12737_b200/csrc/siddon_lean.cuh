@@ -11,10 +11,11 @@
 //  * the winning axis is carried as one-hot 0/1 integers: the per-axis state
 //    updates are integer multiply-adds (FMA pipe) instead of ALU selects, and
 //    the reverse-mode sums (G_a, H_a) are FMAs by 0.0/1.0 masks;
-//  * the winner's ray constants (s, d, 1/d) come from a per-thread record in
-//    shared memory indexed by the axis (one LDS.128 + one LDS.64) instead of a
-//    twelve-instruction select tree; the exact-voxel path reads s, d there too,
-//    so the Ray itself is dead inside the loop;
+//  * the winner's ray constants (d, 1/d) come from a per-thread record in
+//    shared memory indexed by the axis (one LDS.128) instead of a select tree,
+//    and the numerator o + k*sp - s from the source-relative plane table; the
+//    exact-voxel path reads s, d from the record too, so the Ray itself is
+//    dead inside the loop;
 //  * each axis keeps the shared-memory byte address of its next-next plane;
 //  * seg > max(T, 1e-12) is the single fast-path test (used and certified
 //    voxel); everything else takes the reference's exact path out of line;
@@ -25,8 +26,10 @@
 
 namespace drr {
 
-// Per-thread shared-memory record: {s_a, d_a} (16 B) and 1/d_a (8 B) per
-// axis, structure-of-arrays over the CTA's threads (conflict-free LDS.128).
+// Per-thread shared-memory record: {d_a, 1/d_a} (16 B) and s_a (8 B, exact
+// path only) per axis, structure-of-arrays over the CTA's threads
+// (conflict-free LDS.128).  The plane table is source-relative
+// (build_plane_table), so a voxel-step reads {d, 1/d} and the numerator.
 // Walk tuning, per mode (A/B on C2, see profiles/):
 //  * kQ: the record also holds each axis's plane-table cursor and its strides
 //    ({1/d, table step, voxel byte step} 16 B, cursor 4 B), so the winner's
@@ -175,14 +178,17 @@ __device__ __forceinline__ double gather_voxel(const double* p) { return __ldg(p
 // Returns the address to gather (the zero voxel for a skipped segment).
 template <typename VT>
 __device__ __forceinline__ const VT* lean_exact(const VT* __restrict__ vol, const GridDev& g,
-                                                uint32_t sd_s, uint32_t sd_stride, double prev,
-                                                double cur, double seg, int& used) {
+                                                uint32_t dv_s, uint32_t dv_stride, uint32_t sv_s,
+                                                uint32_t sv_stride, double prev, double cur,
+                                                double seg, int& used) {
   used = seg > kSegEps;
   if (!used) return reinterpret_cast<const VT*>(&g_zero_voxel);
-  double s0, d0, s1, d1, s2, d2;
-  lds_2f64(sd_s, s0, d0);
-  lds_2f64(sd_s + sd_stride, s1, d1);
-  lds_2f64(sd_s + 2 * sd_stride, s2, d2);
+  double d0, d1, d2, i0, i1, i2;
+  lds_2f64(dv_s, d0, i0);
+  lds_2f64(dv_s + dv_stride, d1, i1);
+  lds_2f64(dv_s + 2 * dv_stride, d2, i2);
+  const double s0 = lds_f64(sv_s), s1 = lds_f64(sv_s + sv_stride),
+               s2 = lds_f64(sv_s + 2 * sv_stride);
   return vol + exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
 }
 
@@ -204,38 +210,38 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   // range: its midpoint is more than the rounding noise inside every slab)
   const char* bp = reinterpret_cast<const char*>(vol + r.flat);
   // record layout (structure of arrays over the CTA's threads):
-  //   sd[a][tid] = {s_a, d_a}; iv[a][tid] = 1/d_a (+ table step, voxel byte
-  //   step when kQ); qc[a][tid] = table cursor (kQ)
+  //   dv[a][tid] = {d_a, 1/d_a} (the winner's division constants: one
+  //   LDS.128); sv[a][tid] = s_a (exact path only); (kQ) sp[a][tid] =
+  //   {table step, voxel byte step}, qc[a][tid] = table cursor
   constexpr int nt = kLeanThreads;
-  double* sd = rec + 2 * threadIdx.x;
+  double* dv = rec + 2 * threadIdx.x;
+  double* sv = rec + 6 * nt + threadIdx.x;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    sd[2 * a * nt] = r.s[a];
-    sd[2 * a * nt + 1] = r.d[a];
+    dv[2 * a * nt] = r.d[a];
+    dv[2 * a * nt + 1] = r.inv[a];
+    sv[a * nt] = r.s[a];
   }
-  const uint32_t sd_s = static_cast<uint32_t>(__cvta_generic_to_shared(sd));
-  constexpr uint32_t sd_stride = 16u * nt;
-  // (kQ) iv[a][tid] = {1/d, table step, voxel byte step}, qc[a][tid] = cursor;
-  // (!kQ) iv[a][tid] = 1/d, cursors and steps in registers
+  const uint32_t dv_s = static_cast<uint32_t>(__cvta_generic_to_shared(dv));
+  const uint32_t sv_s = static_cast<uint32_t>(__cvta_generic_to_shared(sv));
+  constexpr uint32_t dv_stride = 16u * nt, sv_stride = 8u * nt;
+  // (!kQ) cursors and steps in registers
   uint32_t qa0 = qa_init[0], qa1 = qa_init[1], qa2 = qa_init[2];
   const int qs0 = 8 * r.st[0], qs1 = 8 * r.st[1], qs2 = 8 * r.st[2];
   const int db0 = db_init[0], db1 = db_init[1], db2 = db_init[2];
-  double* iv = rec + 6 * nt + (kQ ? 2 : 1) * threadIdx.x;
+  int* sp = reinterpret_cast<int*>(rec + 9 * nt + threadIdx.x);
   uint32_t* qc = reinterpret_cast<uint32_t*>(rec + 12 * nt) + threadIdx.x;
+  if constexpr (kQ) {
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    if constexpr (kQ) {
-      iv[2 * a * nt] = r.inv[a];
-      reinterpret_cast<int*>(iv + 2 * a * nt + 1)[0] = 8 * r.st[a];
-      reinterpret_cast<int*>(iv + 2 * a * nt + 1)[1] = db_init[a];
+    for (int a = 0; a < 3; ++a) {
+      sp[2 * a * nt] = 8 * r.st[a];
+      sp[2 * a * nt + 1] = db_init[a];
       qc[a * nt] = qa_init[a];
-    } else {
-      iv[a * nt] = r.inv[a];
     }
   }
-  const uint32_t iv_s = static_cast<uint32_t>(__cvta_generic_to_shared(iv));
+  const uint32_t sp_s = static_cast<uint32_t>(__cvta_generic_to_shared(sp));
   const uint32_t qc_s = static_cast<uint32_t>(__cvta_generic_to_shared(qc));
-  constexpr uint32_t iv_stride = (kQ ? 16u : 8u) * nt, qc_stride = 4u * nt;
+  constexpr uint32_t sp_stride = 8u * nt, qc_stride = 4u * nt;
   asm volatile("" ::: "memory");  // the record stores precede every record load
   const double T2 = fmax(r.T, kSegEps);
   double prev = r.amin;
@@ -265,29 +271,26 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     const int m2 = c2, m1 = c1 && !c2, m0 = !(c1 || c2);
     // advance the winning axis
     const uint32_t k = m1 + 2 * m2;
-    double s, d;
-    lds_2f64(sd_s + k * sd_stride, s, d);
-    double inv, P;
+    double d, inv;
+    lds_2f64(dv_s + k * dv_stride, d, inv);
+    double num;  // (o + k*sp) - s from the source-relative plane table
     int db;
     if constexpr (kQ) {
-      long long steps;  // {table step (low word), voxel byte step (high word)}
-      asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=d"(inv), "=l"(steps)
-                   : "r"(iv_s + k * iv_stride));
-      const int qs = static_cast<int>(steps);
-      db = static_cast<int>(steps >> 32);
+      int qs;  // {table step, voxel byte step}
+      asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qs), "=r"(db)
+                   : "r"(sp_s + k * sp_stride));
       uint32_t qa;
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(qa) : "r"(qc_s + k * qc_stride));
-      P = lds_f64(qa);
+      num = lds_f64(qa);
       asm volatile("st.shared.u32 [%0], %1;" :: "r"(qc_s + k * qc_stride), "r"(qa + qs) : "memory");
     } else {
-      P = lds_f64(m0 * qa0 + m1 * qa1 + m2 * qa2);
-      inv = lds_f64(iv_s + k * iv_stride);
+      num = lds_f64(m0 * qa0 + m1 * qa1 + m2 * qa2);
       qa0 += m0 * qs0;
       qa1 += m1 * qs1;
       qa2 += m2 * qs2;
       db = m0 * db0 + m1 * db1 + m2 * db2;
     }
-    const double an = div_rn(P - s, d, inv);
+    const double an = div_rn(num, d, inv);
     an0 = m0 ? an : an0;
     an1 = m1 ? an : an1;
     an2 = m2 ? an : an2;
@@ -295,7 +298,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     const VT* gp = reinterpret_cast<const VT*>(bp);
     int used = 1;
     const double seg = cur - prev;
-    if (!(seg > T2)) gp = lean_exact(vol, g, sd_s, sd_stride, prev, cur, seg, used);
+    if (!(seg > T2)) gp = lean_exact(vol, g, dv_s, dv_stride, sv_s, sv_stride, prev, cur, seg, used);
     bp += db;
     st[j].v = gather_voxel(gp);
     st[j].used = used;
@@ -332,7 +335,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     const double seg = cur - prev;
     const VT* gp = reinterpret_cast<const VT*>(bp);
     int used = 1;
-    if (!(seg > T2)) gp = lean_exact(vol, g, sd_s, sd_stride, prev, cur, seg, used);
+    if (!(seg > T2)) gp = lean_exact(vol, g, dv_s, dv_stride, sv_s, sv_stride, prev, cur, seg, used);
     LeanStage<VT> last;
     last.a = prev;
     last.v = gather_voxel(gp);

@@ -110,20 +110,28 @@ __host__ __device__ __forceinline__ int plane_base(const GridDev& g, int a) {
                 : (a == 1 ? g.n[0] + 1 + 3 * kPad : g.n[0] + g.n[1] + 2 + 5 * kPad);
 }
 
-__device__ __forceinline__ void build_plane_table(const GridDev& g, double* tab) {
+// The table is source-relative: entry k of axis a holds the numerator of the
+// crossing parameter, (o_a + k*sp_a) - s_a -- the reference's two roundings in
+// its order (_native.pyx:105), so num / d is the same division.  Every ray of
+// a CTA shares the source (one pose per CTA; one source per explicit-ray
+// call), so the walk reads the numerator instead of P and s: one shared-memory
+// load and one add fewer per voxel-step.  Sentinels stay +-1e280 (|s| is far
+// below their ulp).
+__device__ __forceinline__ void build_plane_table(const GridDev& g, const double* __restrict__ src,
+                                                  double* tab) {
   const int l0 = g.n[0] + 1 + 2 * kPad, l1 = g.n[1] + 1 + 2 * kPad,
             l2 = g.n[2] + 1 + 2 * kPad;
   for (int i = threadIdx.x; i < l0 + l1 + l2; i += blockDim.x) {
     int j, n;
-    double o, sp;
-    if (i < l0) { j = i; n = g.n[0]; o = g.o[0]; sp = g.sp[0]; }
-    else if (i < l0 + l1) { j = i - l0; n = g.n[1]; o = g.o[1]; sp = g.sp[1]; }
-    else { j = i - l0 - l1; n = g.n[2]; o = g.o[2]; sp = g.sp[2]; }
+    double o, sp, s;
+    if (i < l0) { j = i; n = g.n[0]; o = g.o[0]; sp = g.sp[0]; s = __ldg(src); }
+    else if (i < l0 + l1) { j = i - l0; n = g.n[1]; o = g.o[1]; sp = g.sp[1]; s = __ldg(src + 1); }
+    else { j = i - l0 - l1; n = g.n[2]; o = g.o[2]; sp = g.sp[2]; s = __ldg(src + 2); }
     const int k = j - kPad;
     double v;
     if (k < 0) v = -kSentinel;
     else if (k > n) v = kSentinel;
-    else v = o + static_cast<double>(k) * sp;
+    else v = (o + static_cast<double>(k) * sp) - s;
     tab[i] = v;
   }
 }
@@ -397,11 +405,10 @@ __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
     pipe[DRR_PIPE - 1] = PipeStage<VT>{used, seg, prev, lab, v};
     prev = cur;
     if (last) break;
-    const double s = c2 ? s2 : (c1 ? s1 : s0);
     const double d = c2 ? d2 : (c1 ? d1 : d0);
     const double inv = c2 ? i2 : (c1 ? i1 : i0);
     const int q = (c2 ? q2 : (c1 ? q1 : q0)) + (c2 ? st2 : (c1 ? st1 : st0));
-    const double num = tab[q] - s;
+    const double num = tab[q];  // (o + q*sp) - s: the source-relative table
     const double an = safe ? num / d : div_rn(num, d, inv);
     const bool a0 = !(c1 || c2), a1 = c1 && !c2;
     an0 = a0 ? an : an0;
