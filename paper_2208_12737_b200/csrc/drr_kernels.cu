@@ -35,12 +35,16 @@
 namespace drr {
 
 // Launch bounds (A/B on C2, 32 poses; scripts/gpu_ab.sh, gpu_ab_fast.sh): the
-// gradient walks (k_forward_jac, k_backward) at 5 CTAs/SM with a 3-deep
-// gather pipeline and the forward at 6 CTAs/SM with a 4-deep one were the
-// fastest combinations (2.56 ms / 2.08 ms for 32 poses); ptxas spills only
-// outside the walk's fast path.
+// forward at 6 CTAs/SM with a 4-deep gather pipeline, k_forward_jac at 6 with
+// a 3-deep one (its derived-axis loop fits 80 registers once the walk's end
+// state is parked in shared memory and the direction re-read after it), the
+// re-walk k_backward at 5 (it spills at 6): 1.97 / 2.29 / 2.53 ms for 32
+// poses; ptxas spills only outside the walk's fast path.
 #ifndef DRR_BWD_MINB
 #define DRR_BWD_MINB 5
+#endif
+#ifndef DRR_FJ_MINB
+#define DRR_FJ_MINB 6
 #endif
 #ifndef DRR_FWD_MINB
 #define DRR_FWD_MINB 6
@@ -113,6 +117,26 @@ __device__ __forceinline__ void pixel_ray(const double* __restrict__ f,
     s[a] = __ldg(f + a);
     p[a] = (__ldg(f + 3 + a) + ah * __ldg(f + 6 + a)) + aw * __ldg(f + 9 + a);
   }
+}
+
+// The direction p - s of pixel (h, w), re-read from the frames after a walk
+// (volatile loads, so the compiler cannot keep the pre-walk values alive
+// across the walk loop instead: registers there are what bound occupancy).
+// Same operations as pixel_ray + ray_setup, so bit-identical.
+__device__ __forceinline__ void reload_ray_d(const double* __restrict__ f, const DetDev& det,
+                                             int h, int w, double* d) {
+  const double ah = (static_cast<double>(h) - det.half_h) * det.pitch_y;
+  const double aw = (static_cast<double>(w) - det.half_w) * det.pitch_x;
+  double v[12];
+#pragma unroll
+  for (int i = 0; i < 12; ++i)
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v[i]) : "l"(f + i));
+#pragma unroll
+  for (int a = 0; a < 3; ++a) d[a] = ((v[3 + a] + ah * v[6 + a]) + aw * v[9 + a]) - v[a];
+}
+
+__device__ __forceinline__ double ray_length(const double* d) {
+  return sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
 }
 
 __device__ __forceinline__ double ray_length(const Ray& r) {
@@ -195,20 +219,25 @@ __global__ void __launch_bounds__(kThreads)
 
 // Endpoint gradients from summed walk totals (acc, G, H): the same algebra as
 // endpoint_grads, for chunked walks whose partial sums were combined.
-__device__ __forceinline__ void sums_to_endpoint_grads(const Ray& r, double acc,
+__device__ __forceinline__ void sums_to_endpoint_grads(const double* d, double acc,
                                                        const double* G, const double* Hh,
                                                        double L, double* dEds, double* dEdp) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double gs = 0.0, gp = 0.0;
-    if (r.d[a] != 0.0) {
-      gs = L * (Hh[a] - G[a]) / r.d[a];
-      gp = -L * Hh[a] / r.d[a];
+    if (d[a] != 0.0) {
+      gs = L * (Hh[a] - G[a]) / d[a];
+      gp = -L * Hh[a] / d[a];
     }
-    const double lt = r.d[a] / L * acc;
+    const double lt = d[a] / L * acc;
     dEds[a] = gs - lt;
     dEdp[a] = gp + lt;
   }
+}
+__device__ __forceinline__ void sums_to_endpoint_grads(const Ray& r, double acc,
+                                                       const double* G, const double* Hh,
+                                                       double L, double* dEds, double* dEdp) {
+  sums_to_endpoint_grads(r.d, acc, G, Hh, L, dEds, dEdp);
 }
 
 // --------------------------------------------------------------- backward
@@ -302,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
 // derivatives are stored (SoA, jac[c * npix_total + pix], f64) and
 // k_backward_jac contracts them with it -- no second walk of the CT.
 template <typename VT, typename OT, int K>
-__global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
+__global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
     k_forward_jac(const VT* __restrict__ vol, const GridDev g,
                   const double* __restrict__ frames, const DetDev det,
                   OT* __restrict__ img, double* __restrict__ jac, size_t npix_total) {
@@ -333,11 +362,13 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
   for (int k = 0; k < 7; ++k) part[k] = chunk_sum<K>(part[k]);
   if (valid && chunk == 0) {
     const size_t pix = (static_cast<size_t>(b) * det.H + h) * det.W + w;
-    const double L = ray_length(r);
+    double d[3];
+    reload_ray_d(frames + 12 * b, det, h, w, d);
+    const double L = ray_length(d);
     double dEds[3] = {0.0, 0.0, 0.0}, dEdp[3] = {0.0, 0.0, 0.0};
     if (part[0] != 0.0 || part[1] != 0.0 || part[2] != 0.0 || part[3] != 0.0 ||
         part[4] != 0.0 || part[5] != 0.0 || part[6] != 0.0)
-      sums_to_endpoint_grads(r, part[0], part + 1, part + 4, L, dEds, dEdp);
+      sums_to_endpoint_grads(d, part[0], part + 1, part + 4, L, dEds, dEdp);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       jac[a * npix_total + pix] = dEds[a];

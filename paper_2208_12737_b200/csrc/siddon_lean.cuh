@@ -50,11 +50,12 @@ namespace drr {
 #ifndef DRR_LEAN_Q_GRAD
 #define DRR_LEAN_Q_GRAD 1
 #endif
-constexpr int kLeanRecDoublesPerThread = 14;  // the largest record (kQ)
-// Record doubles per thread a walk mode uses: {s, d} x 3 and 1/d x 3, plus
-// (kQ) the steps next to 1/d and the 3 table cursors.
+constexpr int kLeanRecDoublesPerThread = 15;  // the largest record (gradient walk)
+// Record doubles per thread a walk mode uses: {d, 1/d} x 3 and s x 3, plus
+// (kQ) the table / voxel steps and the 3 table cursors, plus (gradient walk)
+// the walk's end parameter and labels, parked there for the loop's duration.
 __host__ __device__ constexpr int lean_rec_doubles(bool grad_walk) {
-  return (grad_walk ? DRR_LEAN_Q_GRAD : DRR_LEAN_Q_FWD) ? 14 : 9;
+  return grad_walk ? 15 : (DRR_LEAN_Q_FWD ? 14 : 9);
 }
 constexpr int kLeanThreads = 128;  // threads per CTA of every kernel using the walk
 
@@ -239,6 +240,14 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
       qc[a * nt] = qa_init[a];
     }
   }
+  // (gradient walk) the end parameter and labels are only needed after the
+  // loop: park them in the record instead of holding registers across it
+  double* park_a = rec + 14 * nt + threadIdx.x;
+  uint32_t* park_l = qc + 3 * nt;
+  if constexpr (kMode == kLeanGrad) {
+    *park_a = r.amax;
+    *park_l = static_cast<uint32_t>(r.lab_max) | (static_cast<uint32_t>(r.D) << 8);
+  }
   const uint32_t sp_s = static_cast<uint32_t>(__cvta_generic_to_shared(sp));
   const uint32_t qc_s = static_cast<uint32_t>(__cvta_generic_to_shared(qc));
   constexpr uint32_t sp_stride = 8u * nt, qc_stride = 4u * nt;
@@ -330,8 +339,19 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   for (int j = 0; j + 1 < kLeanPipe; ++j)
     if (j < rem) lean_consume<kMode, kDerive, VT>(o, pend, st[j], j + 1 < rem ? st[j + 1].a : prev);
   // final segment [last crossing, amax]
+  double amax = r.amax;
+  int lab_max = r.lab_max, Dax = r.D;
+  if constexpr (kMode == kLeanGrad) {
+    uint32_t pl;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(amax)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(park_a))));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pl)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(park_l))));
+    lab_max = static_cast<int>(pl & 0xFFu);
+    Dax = static_cast<int>(pl >> 8);
+  }
   {
-    const double cur = r.amax;
+    const double cur = amax;
     const double seg = cur - prev;
     const VT* gp = reinterpret_cast<const VT*>(bp);
     int used = 1;
@@ -345,19 +365,19 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   }
   if constexpr (kMode == kLeanGrad) {
     if constexpr (kDerive) {
-      lean_apply<true>(o, derive_mask(r.lab_max), r.amax, pend);
-      const double gc = r.lab_max == kConstLabel ? pend : 0.0;
-      const double hc = r.lab_max == kConstLabel ? pend * r.amax : 0.0;
+      lean_apply<true>(o, derive_mask(lab_max), amax, pend);
+      const double gc = lab_max == kConstLabel ? pend : 0.0;
+      const double hc = lab_max == kConstLabel ? pend * amax : 0.0;
       const double gA = o.G0, gB = o.G1, hA = o.H0, hB = o.H1;
       const double gD = -((gA + gB) + gc), hD = ((o.acc - hA) - hB) - hc;
-      o.G0 = r.D == 0 ? gD : gA;
-      o.H0 = r.D == 0 ? hD : hA;
-      o.G1 = r.D == 1 ? gD : (r.D == 0 ? gA : gB);
-      o.H1 = r.D == 1 ? hD : (r.D == 0 ? hA : hB);
-      o.G2 = r.D == 2 ? gD : gB;
-      o.H2 = r.D == 2 ? hD : hB;
+      o.G0 = Dax == 0 ? gD : gA;
+      o.H0 = Dax == 0 ? hD : hA;
+      o.G1 = Dax == 1 ? gD : (Dax == 0 ? gA : gB);
+      o.H1 = Dax == 1 ? hD : (Dax == 0 ? hA : hB);
+      o.G2 = Dax == 2 ? gD : gB;
+      o.H2 = Dax == 2 ? hD : hB;
     } else {
-      lean_apply<false>(o, lab_mask(r.lab_max), r.amax, pend);
+      lean_apply<false>(o, lab_mask(lab_max), amax, pend);
     }
   }
 }
