@@ -72,19 +72,45 @@ struct Tile {
   static constexpr int H = K == 1 ? kQuadH * kCtaQuadsH : 16 / K;
 };
 
+// Which (tile, pose) a CTA of a pose launch renders.  The grid is (tiles x,
+// tiles y, poses); with DRR_POSE_FAST the CTA's linear launch index is
+// re-read pose-fastest, so the CTAs resident at any moment cover one band of
+// detector tiles for every pose of the batch rather than the whole detector
+// of a few poses: the rays in flight then cross the same part of the CT
+// (nearby poses), and the CT lines they gather stay in L2.  Only the work
+// assignment changes; every ray and every partial lands where it did.
+#ifndef DRR_POSE_FAST
+#define DRR_POSE_FAST 1
+#endif
+struct CtaPos {
+  int tx, ty, b;
+};
+__device__ __forceinline__ CtaPos cta_pos() {
+#if DRR_POSE_FAST
+  const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const unsigned tile = lin / gridDim.z;
+  return CtaPos{static_cast<int>(tile % gridDim.x), static_cast<int>(tile / gridDim.x),
+                static_cast<int>(lin % gridDim.z)};
+#else
+  return CtaPos{static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.y),
+                static_cast<int>(blockIdx.z)};
+#endif
+}
+
 template <int K>
 __device__ __forceinline__ void tile_ray(int& h, int& w, int& chunk) {
+  const CtaPos c = cta_pos();
   const int t = threadIdx.x;
   if (K == 1) {
     const int warp = t >> 5, lane = t & 31;
-    w = blockIdx.x * Tile<K>::W + (warp % kCtaQuadsW) * kQuadW + (lane % kQuadW);
-    h = blockIdx.y * Tile<K>::H + (warp / kCtaQuadsW) * kQuadH + (lane / kQuadW);
+    w = c.tx * Tile<K>::W + (warp % kCtaQuadsW) * kQuadW + (lane % kQuadW);
+    h = c.ty * Tile<K>::H + (warp / kCtaQuadsW) * kQuadH + (lane / kQuadW);
     chunk = 0;
   } else {
     const int ray = t / K;
     chunk = t % K;
-    w = blockIdx.x * Tile<K>::W + (ray & 7);
-    h = blockIdx.y * Tile<K>::H + (ray >> 3);
+    w = c.tx * Tile<K>::W + (ray & 7);
+    h = c.ty * Tile<K>::H + (ray >> 3);
   }
 }
 
@@ -163,13 +189,13 @@ __global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FWD_MINB : DRR_SPLIT_MI
               const double* __restrict__ frames, const DetDev det,
               OT* __restrict__ img) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, frames + 12 * blockIdx.z, tab);  // s of this CTA's pose
+  build_plane_table(g, frames + 12 * cta_pos().b, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
   tile_ray<K>(h, w, chunk);
   const bool valid = h < det.H && w < det.W;
   if (K == 1 && !valid) return;
-  const int b = blockIdx.z;
+  const int b = cta_pos().b;
   double acc = 0.0, L = 0.0;
   if (valid) {
     double s[3], p[3], ah, aw;
@@ -194,13 +220,13 @@ __global__ void __launch_bounds__(kThreads)
             const double* __restrict__ frames, const DetDev det,
             int* __restrict__ steps) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, frames + 12 * blockIdx.z, tab);  // s of this CTA's pose
+  build_plane_table(g, frames + 12 * cta_pos().b, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
   tile_ray<K>(h, w, chunk);
   const bool valid = h < det.H && w < det.W;
   if (K == 1 && !valid) return;
-  const int b = blockIdx.z;
+  const int b = cta_pos().b;
   int n = 0;
   if (valid) {
     double s[3], p[3], ah, aw;
@@ -248,11 +274,11 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
                const GT* __restrict__ grad_img, OT* __restrict__ img,
                double* __restrict__ partials) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, frames + 12 * blockIdx.z, tab);  // s of this CTA's pose
+  build_plane_table(g, frames + 12 * cta_pos().b, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
   tile_ray<K>(h, w, chunk);
-  const int b = blockIdx.z;
+  const int b = cta_pos().b;
   const bool valid = h < det.H && w < det.W;
   double acc12[kFrameGrads];
 #pragma unroll
@@ -316,7 +342,8 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
 #pragma unroll
     for (int q = 0; q < kThreads / 32; ++q) v += warp_part[q][threadIdx.x];
     const int blocks_per_pose = gridDim.x * gridDim.y;
-    const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+    const CtaPos c = cta_pos();
+    const int blk = c.ty * gridDim.x + c.tx;
     partials[(static_cast<size_t>(b) * blocks_per_pose + blk) * kFrameGrads +
              threadIdx.x] = v;
   }
@@ -336,13 +363,13 @@ __global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
                   const double* __restrict__ frames, const DetDev det,
                   OT* __restrict__ img, double* __restrict__ jac, size_t npix_total) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, frames + 12 * blockIdx.z, tab);  // s of this CTA's pose
+  build_plane_table(g, frames + 12 * cta_pos().b, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
   tile_ray<K>(h, w, chunk);
   const bool valid = h < det.H && w < det.W;
   if (K == 1 && !valid) return;
-  const int b = blockIdx.z;
+  const int b = cta_pos().b;
   double part[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   double s[3], p[3], ah = 0.0, aw = 0.0;
   Ray r;
@@ -387,7 +414,7 @@ __global__ void __launch_bounds__(kThreads)
                    const GT* __restrict__ grad_img, double* __restrict__ partials) {
   int h, w, chunk;
   tile_ray<1>(h, w, chunk);
-  const int b = blockIdx.z;
+  const int b = cta_pos().b;
   double acc12[kFrameGrads];
 #pragma unroll
   for (int k = 0; k < kFrameGrads; ++k) acc12[k] = 0.0;
@@ -433,7 +460,8 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int q = 0; q < kThreads / 32; ++q) v += warp_part[q][threadIdx.x];
     const int blocks_per_pose = gridDim.x * gridDim.y;
-    const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+    const CtaPos c = cta_pos();
+    const int blk = c.ty * gridDim.x + c.tx;
     partials[(static_cast<size_t>(b) * blocks_per_pose + blk) * kFrameGrads +
              threadIdx.x] = v;
   }

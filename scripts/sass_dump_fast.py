@@ -11,14 +11,16 @@ for part in re.split(r'\n\s*Function : ', text)[1:]:
          if re.match(r'\s*/\*[0-9a-f]{4,5}\*/', l)]
     A = [int(re.match(r'/\*([0-9a-f]+)\*/', l).group(1), 16) for l in L]
     pos = {a: i for i, a in enumerate(A)}
-    best = None
+    loops = []
     for i, l in enumerate(L):
         m = re.search(r'BRA (0x[0-9a-f]+)', l)
         if m:
             t = int(m.group(1), 16)
-            if t < A[i] and (best is None or A[i] - t > best[1] - best[0]):
-                best = (t, A[i], i)
-    t0, t1, iend = best
+            if t < A[i]:
+                loops.append((t, A[i], i))
+    # argv[3]: which loop, by size rank (0 = the largest)
+    loops.sort(key=lambda x: x[0] - x[1])
+    t0, t1, iend = loops[int(sys.argv[3]) if len(sys.argv) > 3 else 0]
     i = pos[t0]
     while i <= iend:
         l = L[i]
