@@ -90,10 +90,11 @@ __device__ __forceinline__ LabMask lab_mask(int lab) {
   return LabMask{lab == 0 ? kOneHi : 0, lab == 1 ? kOneHi : 0, lab == 2 ? kOneHi : 0};
 }
 
-// A segment whose gather is in flight: the parameter of its starting crossing
-// (its length is the next stage's parameter minus this one -- the same
-// subtraction the walk made, so bit-identical), the value (0 if skipped), the
-// starting crossing's label and, for counting, the used flag.
+// A segment whose gather is in flight: in the gradient walk the parameter of
+// its starting crossing (its length is the next stage's parameter minus this
+// one -- the same subtraction the walk made, so bit-identical), in the sum walk
+// its length; the value (0 if skipped), the starting crossing's label and, for
+// counting, the used flag.
 template <typename VT>
 struct LeanStage {
   double a = 0.0;
@@ -129,7 +130,9 @@ __device__ __forceinline__ void lean_consume(LeanSums& o, double& pend, const Le
     return;
   }
   const double vv = static_cast<double>(st.v);  // 0 for skipped segments
-  const double seg = a_next - st.a;
+  // the gradient walk re-derives the length (its stage holds the start
+  // parameter, needed for H); the sum walk's stage holds the length itself
+  const double seg = kMode == kLeanGrad ? a_next - st.a : st.a;
   o.acc = o.acc + seg * vv;                       // _native.pyx:187 (TU is --fmad=false)
   if (kMode == kLeanGrad) {
     lean_apply<kDerive>(o, st.m, st.a, pend - vv);
@@ -267,7 +270,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   // Initially every slot is an empty segment [amin, amin) (adds nothing).
   LeanStage<VT> st[kLeanPipe];
 #pragma unroll
-  for (int j = 0; j < kLeanPipe; ++j) st[j].a = prev;
+  for (int j = 0; j < kLeanPipe; ++j) st[j].a = kMode == kLeanGrad ? prev : 0.0;
   // one step: consume ring slot j (the segment issued kLeanPipe steps ago;
   // it ends where slot j+1's segment starts), pick the winning crossing,
   // issue this segment's gather into slot j
@@ -311,7 +314,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     bp += db;
     st[j].v = gather_voxel(gp);
     st[j].used = used;
-    st[j].a = prev;
+    st[j].a = kMode == kLeanGrad ? prev : seg;
     st[j].m = lm;
     if constexpr (kDerive)
       lm = derive_mask(static_cast<int>(k));
@@ -357,7 +360,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     int used = 1;
     if (!(seg > T2)) gp = lean_exact(vol, g, dv_s, dv_stride, sv_s, sv_stride, prev, cur, seg, used);
     LeanStage<VT> last;
-    last.a = prev;
+    last.a = kMode == kLeanGrad ? prev : seg;
     last.v = gather_voxel(gp);
     last.used = used;
     last.m = lm;
