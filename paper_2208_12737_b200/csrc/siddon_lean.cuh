@@ -50,6 +50,12 @@ namespace drr {
 #ifndef DRR_LEAN_Q_GRAD
 #define DRR_LEAN_Q_GRAD 1
 #endif
+// kQ record entry per axis: 1 = {table cursor, voxel byte step} in one 8-byte
+// word (one load; the table step, +-8, follows from the voxel step's sign);
+// 0 = {table step, voxel byte step} and the cursor in a separate word.
+#ifndef DRR_LEAN_QPACK
+#define DRR_LEAN_QPACK 1
+#endif
 constexpr int kLeanRecDoublesPerThread = 15;  // the largest record (gradient walk)
 // Record doubles per thread a walk mode uses: {d, 1/d} x 3 and s x 3, plus
 // (kQ) the table / voxel steps and the 3 table cursors, plus (gradient walk)
@@ -238,9 +244,9 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   if constexpr (kQ) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      sp[2 * a * nt] = 8 * r.st[a];
+      sp[2 * a * nt] = DRR_LEAN_QPACK ? static_cast<int>(qa_init[a]) : 8 * r.st[a];
       sp[2 * a * nt + 1] = db_init[a];
-      qc[a * nt] = qa_init[a];
+      if (!DRR_LEAN_QPACK) qc[a * nt] = qa_init[a];
     }
   }
   // (gradient walk) the end parameter and labels are only needed after the
@@ -287,7 +293,14 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     lds_2f64(dv_s + k * dv_stride, d, inv);
     double num;  // (o + k*sp) - s from the source-relative plane table
     int db;
-    if constexpr (kQ) {
+    if constexpr (kQ && DRR_LEAN_QPACK) {
+      uint32_t qa;  // {table cursor, voxel byte step}
+      asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qa), "=r"(db)
+                   : "r"(sp_s + k * sp_stride));
+      num = lds_f64(qa);
+      const uint32_t qs = 8u + (static_cast<uint32_t>(db >> 31) << 4);  // +-8 by the walk's sign
+      asm volatile("st.shared.u32 [%0], %1;" :: "r"(sp_s + k * sp_stride), "r"(qa + qs) : "memory");
+    } else if constexpr (kQ) {
       int qs;  // {table step, voxel byte step}
       asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qs), "=r"(db)
                    : "r"(sp_s + k * sp_stride));
