@@ -87,7 +87,12 @@ struct LeanSums {
 #endif
 
 // Label of a crossing as the high words of three 0.0/1.0 doubles (one-hot over
-// the axes; label 3 = clip: all zero, no tangent).
+// the axes; label 3 = clip: all zero, no tangent).  With DRR_LEAN_LAB1 the
+// derived-axis walk keeps the bare axis id in h0 instead and forms the two
+// masks where they are used (one register per stage, no mask copies).
+#ifndef DRR_LEAN_LAB1
+#define DRR_LEAN_LAB1 1
+#endif
 struct LabMask {
   int h0, h1, h2;
 };
@@ -113,9 +118,13 @@ struct LeanStage {
 // branch and no select tree (c * 1 and c * 0 are exact; H rounds c * alpha
 // once before the add, ~1 ulp of one term; the oracle bar is 1e-10 relative).
 template <bool kDerive>
-__device__ __forceinline__ void lean_apply(LeanSums& o, const LabMask& m, double a, double c) {
+__device__ __forceinline__ void lean_apply(LeanSums& o, const LabMask& m, double a, double c,
+                                           int axA = 0, int axB = 0) {
   const double ca = c * a;
-  const double k0 = __hiloint2double(m.h0, 0), k1 = __hiloint2double(m.h1, 0);
+  constexpr bool kLab1 = kDerive && DRR_LEAN_LAB1;
+  const int h0 = kLab1 ? (m.h0 == axA ? kOneHi : 0) : m.h0;
+  const int h1 = kLab1 ? (m.h0 == axB ? kOneHi : 0) : m.h1;
+  const double k0 = __hiloint2double(h0, 0), k1 = __hiloint2double(h1, 0);
   o.G0 = __fma_rn(c, k0, o.G0);
   o.G1 = __fma_rn(c, k1, o.G1);
   o.H0 = __fma_rn(ca, k0, o.H0);
@@ -130,7 +139,7 @@ __device__ __forceinline__ void lean_apply(LeanSums& o, const LabMask& m, double
 // Consume one segment: [a, a_next) with value v.
 template <int kMode, bool kDerive, typename VT>
 __device__ __forceinline__ void lean_consume(LeanSums& o, double& pend, const LeanStage<VT>& st,
-                                             double a_next) {
+                                             double a_next, int axA = 0, int axB = 0) {
   if (kMode == kLeanCount) {
     o.steps += st.used;
     return;
@@ -141,7 +150,7 @@ __device__ __forceinline__ void lean_consume(LeanSums& o, double& pend, const Le
   const double seg = kMode == kLeanGrad ? a_next - st.a : st.a;
   o.acc = o.acc + seg * vv;                       // _native.pyx:187 (TU is --fmad=false)
   if (kMode == kLeanGrad) {
-    lean_apply<kDerive>(o, st.m, st.a, pend - vv);
+    lean_apply<kDerive>(o, st.m, st.a, pend - vv, axA, axB);
     pend = vv;
   }
 }
@@ -266,6 +275,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   // non-dominant axes (kDerive): masks h0 = [axis == A], h1 = [axis == B]
   const int axA = r.D == 0 ? 1 : 0, axB = r.D == 2 ? 1 : 2;
   auto derive_mask = [&](int lab) {
+    if (DRR_LEAN_LAB1) return LabMask{lab, 0, 0};
     return LabMask{lab == axA ? kOneHi : 0, lab == axB ? kOneHi : 0, 0};
   };
   LabMask lm = kDerive ? derive_mask(r.lab_min) : lab_mask(r.lab_min);  // crossing at prev
@@ -281,7 +291,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   // it ends where slot j+1's segment starts), pick the winning crossing,
   // issue this segment's gather into slot j
   auto step = [&](int j) {
-    lean_consume<kMode, kDerive, VT>(o, pend, st[j], st[(j + 1) % kLeanPipe].a);
+    lean_consume<kMode, kDerive, VT>(o, pend, st[j], st[(j + 1) % kLeanPipe].a, axA, axB);
     const bool c1 = an1 < an0;  // ties go to the lowest axis (_native.pyx:180-183)
     const double b01 = c1 ? an1 : an0;
     const bool c2 = an2 < b01;
@@ -350,10 +360,12 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   for (int j = 0; j < kLeanPipe; ++j)
     if (j >= rem)
       lean_consume<kMode, kDerive, VT>(o, pend, st[j],
-                              j + 1 < kLeanPipe ? st[j + 1].a : (rem > 0 ? st[0].a : prev));
+                              j + 1 < kLeanPipe ? st[j + 1].a : (rem > 0 ? st[0].a : prev), axA,
+                              axB);
 #pragma unroll
   for (int j = 0; j + 1 < kLeanPipe; ++j)
-    if (j < rem) lean_consume<kMode, kDerive, VT>(o, pend, st[j], j + 1 < rem ? st[j + 1].a : prev);
+    if (j < rem)
+      lean_consume<kMode, kDerive, VT>(o, pend, st[j], j + 1 < rem ? st[j + 1].a : prev, axA, axB);
   // final segment [last crossing, amax]
   double amax = r.amax;
   int lab_max = r.lab_max, Dax = r.D;
@@ -377,11 +389,11 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     last.v = gather_voxel(gp);
     last.used = used;
     last.m = lm;
-    lean_consume<kMode, kDerive, VT>(o, pend, last, cur);
+    lean_consume<kMode, kDerive, VT>(o, pend, last, cur, axA, axB);
   }
   if constexpr (kMode == kLeanGrad) {
     if constexpr (kDerive) {
-      lean_apply<true>(o, derive_mask(lab_max), amax, pend);
+      lean_apply<true>(o, derive_mask(lab_max), amax, pend, axA, axB);
       const double gc = lab_max == kConstLabel ? pend : 0.0;
       const double hc = lab_max == kConstLabel ? pend * amax : 0.0;
       const double gA = o.G0, gB = o.G1, hA = o.H0, hB = o.H1;
