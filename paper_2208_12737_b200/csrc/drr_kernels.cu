@@ -72,34 +72,49 @@ struct Tile {
   static constexpr int H = K == 1 ? kQuadH * kCtaQuadsH : 16 / K;
 };
 
+struct DetDev {
+  int H, W;
+  int split;       // requested threads per ray (0 = auto)
+  int pose_group;  // poses interleaved tile by tile in the CTA order (>= 1)
+  double pitch_x, pitch_y;
+  double half_h, half_w;  // (H-1)/2.0, (W-1)/2.0   (geometry.py:155-156)
+};
+
 // Which (tile, pose) a CTA of a pose launch renders.  The grid is (tiles x,
-// tiles y, poses); with DRR_POSE_FAST the CTA's linear launch index is
-// re-read pose-fastest, so the CTAs resident at any moment cover one band of
-// detector tiles for every pose of the batch rather than the whole detector
-// of a few poses: the rays in flight then cross the same part of the CT
-// (nearby poses), and the CT lines they gather stay in L2.  Only the work
-// assignment changes; every ray and every partial lands where it did.
-#ifndef DRR_POSE_FAST
-#define DRR_POSE_FAST 1
-#endif
+// tiles y, poses); the CTA's linear launch index is re-read with the poses of
+// a group of det.pose_group fastest, then the tiles, then the groups.  With
+// a group spanning the batch, the CTAs resident at any moment cover one band
+// of detector tiles for every pose rather than the whole detector of a few
+// poses: nearby poses cross the same part of the CT, whose lines then stay in
+// L2.  Only the work assignment changes; every ray and every partial lands
+// where it did.
 struct CtaPos {
   int tx, ty, b;
 };
-__device__ __forceinline__ CtaPos cta_pos() {
-#if DRR_POSE_FAST
-  const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  const unsigned tile = lin / gridDim.z;
+// (the indices are read with volatile moves, so a kernel can recompute its
+// pixel after the walk instead of holding it in registers across the loop)
+__device__ __forceinline__ unsigned sreg_ctaid(int a) {
+  unsigned v;
+  if (a == 0) asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(v));
+  else if (a == 1) asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(v));
+  else asm volatile("mov.u32 %0, %%ctaid.z;" : "=r"(v));
+  return v;
+}
+__device__ __forceinline__ CtaPos cta_pos(const DetDev& det) {
+  const unsigned lin = sreg_ctaid(0) + gridDim.x * (sreg_ctaid(1) + gridDim.y * sreg_ctaid(2));
+  const unsigned tiles = gridDim.x * gridDim.y, B = gridDim.z;
+  const unsigned G = static_cast<unsigned>(det.pose_group);
+  const unsigned gi = lin / (G * tiles);
+  const unsigned gl = min(G, B - gi * G);  // the last group may be smaller
+  const unsigned rem = lin - gi * G * tiles;
+  const unsigned tile = rem / gl;
   return CtaPos{static_cast<int>(tile % gridDim.x), static_cast<int>(tile / gridDim.x),
-                static_cast<int>(lin % gridDim.z)};
-#else
-  return CtaPos{static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.y),
-                static_cast<int>(blockIdx.z)};
-#endif
+                static_cast<int>(gi * G + rem % gl)};
 }
 
 template <int K>
-__device__ __forceinline__ void tile_ray(int& h, int& w, int& chunk) {
-  const CtaPos c = cta_pos();
+__device__ __forceinline__ void tile_ray(const DetDev& det, int& h, int& w, int& chunk) {
+  const CtaPos c = cta_pos(det);
   const int t = threadIdx.x;
   if (K == 1) {
     const int warp = t >> 5, lane = t & 31;
@@ -122,12 +137,6 @@ __device__ __forceinline__ T chunk_sum(T x) {
   return x;
 }
 
-struct DetDev {
-  int H, W;
-  int split;  // requested threads per ray (0 = auto)
-  double pitch_x, pitch_y;
-  double half_h, half_w;  // (H-1)/2.0, (W-1)/2.0   (geometry.py:155-156)
-};
 
 // Pixel position (c + a_h e1) + a_w e2 in numpy's evaluation order
 // (geometry.py:171-174); the TU is built --fmad=false, so this rounds
@@ -189,13 +198,13 @@ __global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FWD_MINB : DRR_SPLIT_MI
               const double* __restrict__ frames, const DetDev det,
               OT* __restrict__ img) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, frames + 12 * cta_pos().b, tab);  // s of this CTA's pose
+  build_plane_table(g, frames + 12 * cta_pos(det).b, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
-  tile_ray<K>(h, w, chunk);
+  tile_ray<K>(det, h, w, chunk);
   const bool valid = h < det.H && w < det.W;
   if (K == 1 && !valid) return;
-  const int b = cta_pos().b;
+  const int b = cta_pos(det).b;
   double acc = 0.0, L = 0.0;
   if (valid) {
     double s[3], p[3], ah, aw;
@@ -220,13 +229,13 @@ __global__ void __launch_bounds__(kThreads)
             const double* __restrict__ frames, const DetDev det,
             int* __restrict__ steps) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, frames + 12 * cta_pos().b, tab);  // s of this CTA's pose
+  build_plane_table(g, frames + 12 * cta_pos(det).b, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
-  tile_ray<K>(h, w, chunk);
+  tile_ray<K>(det, h, w, chunk);
   const bool valid = h < det.H && w < det.W;
   if (K == 1 && !valid) return;
-  const int b = cta_pos().b;
+  const int b = cta_pos(det).b;
   int n = 0;
   if (valid) {
     double s[3], p[3], ah, aw;
@@ -274,11 +283,11 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
                const GT* __restrict__ grad_img, OT* __restrict__ img,
                double* __restrict__ partials) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, frames + 12 * cta_pos().b, tab);  // s of this CTA's pose
+  build_plane_table(g, frames + 12 * cta_pos(det).b, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
-  tile_ray<K>(h, w, chunk);
-  const int b = cta_pos().b;
+  tile_ray<K>(det, h, w, chunk);
+  const int b = cta_pos(det).b;
   const bool valid = h < det.H && w < det.W;
   double acc12[kFrameGrads];
 #pragma unroll
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
 #pragma unroll
     for (int q = 0; q < kThreads / 32; ++q) v += warp_part[q][threadIdx.x];
     const int blocks_per_pose = gridDim.x * gridDim.y;
-    const CtaPos c = cta_pos();
+    const CtaPos c = cta_pos(det);
     const int blk = c.ty * gridDim.x + c.tx;
     partials[(static_cast<size_t>(b) * blocks_per_pose + blk) * kFrameGrads +
              threadIdx.x] = v;
@@ -363,13 +372,13 @@ __global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
                   const double* __restrict__ frames, const DetDev det,
                   OT* __restrict__ img, double* __restrict__ jac, size_t npix_total) {
   extern __shared__ __align__(16) double tab[];
-  build_plane_table(g, frames + 12 * cta_pos().b, tab);  // s of this CTA's pose
+  build_plane_table(g, frames + 12 * cta_pos(det).b, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
-  tile_ray<K>(h, w, chunk);
+  tile_ray<K>(det, h, w, chunk);
   const bool valid = h < det.H && w < det.W;
   if (K == 1 && !valid) return;
-  const int b = cta_pos().b;
+  const int b = cta_pos(det).b;
   double part[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   double s[3], p[3], ah = 0.0, aw = 0.0;
   Ray r;
@@ -387,10 +396,13 @@ __global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
   }
 #pragma unroll
   for (int k = 0; k < 7; ++k) part[k] = chunk_sum<K>(part[k]);
-  if (valid && chunk == 0) {
-    const size_t pix = (static_cast<size_t>(b) * det.H + h) * det.W + w;
+  // the pixel again (volatile index reads): nothing of it is held across the walk
+  tile_ray<K>(det, h, w, chunk);
+  const int bp = cta_pos(det).b;
+  if (h < det.H && w < det.W && chunk == 0) {
+    const size_t pix = (static_cast<size_t>(bp) * det.H + h) * det.W + w;
     double d[3];
-    reload_ray_d(frames + 12 * b, det, h, w, d);
+    reload_ray_d(frames + 12 * bp, det, h, w, d);
     const double L = ray_length(d);
     double dEds[3] = {0.0, 0.0, 0.0}, dEdp[3] = {0.0, 0.0, 0.0};
     if (part[0] != 0.0 || part[1] != 0.0 || part[2] != 0.0 || part[3] != 0.0 ||
@@ -413,8 +425,8 @@ __global__ void __launch_bounds__(kThreads)
     k_backward_jac(const double* __restrict__ jac, size_t npix_total, const DetDev det,
                    const GT* __restrict__ grad_img, double* __restrict__ partials) {
   int h, w, chunk;
-  tile_ray<1>(h, w, chunk);
-  const int b = cta_pos().b;
+  tile_ray<1>(det, h, w, chunk);
+  const int b = cta_pos(det).b;
   double acc12[kFrameGrads];
 #pragma unroll
   for (int k = 0; k < kFrameGrads; ++k) acc12[k] = 0.0;
@@ -460,7 +472,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int q = 0; q < kThreads / 32; ++q) v += warp_part[q][threadIdx.x];
     const int blocks_per_pose = gridDim.x * gridDim.y;
-    const CtaPos c = cta_pos();
+    const CtaPos c = cta_pos(det);
     const int blk = c.ty * gridDim.x + c.tx;
     partials[(static_cast<size_t>(b) * blocks_per_pose + blk) * kFrameGrads +
              threadIdx.x] = v;
@@ -647,6 +659,7 @@ int make_det(const drr_detector* in, drr::DetDev& d) {
   d.H = in->height;
   d.W = in->width;
   d.split = in->ray_split;
+  d.pose_group = 1;
   d.pitch_x = in->pitch_x;
   d.pitch_y = in->pitch_y;
   d.half_h = static_cast<double>(in->height - 1) / 2.0;
@@ -664,7 +677,26 @@ int ray_split(const drr::DetDev& d, int n_poses) {
   return k;
 }
 
-dim3 pose_grid(const drr::DetDev& d, int n_poses, int K) {
+// Poses interleaved tile by tile in the CTA order (DetDev::pose_group):
+// groups of ~16K CTAs (G = 16384 / tiles per pose).  Interleaving pays when a
+// tile's CT footprint is large next to the pose spread (nearby poses share
+// it), and costs when tiles are many and small (each pose then brings its own
+// lines).  A/B (scripts/gpu_ab_fast.sh, gpu_ab_configs.sh; fwd+jac ms or
+// DRR/s for G = 1 / 2 / 4 / 8 / 16 / whole batch):
+//   C2 (32 poses, 325 tiles):    2.40 / 2.35 / 2.30 / 2.25 / 2.24 / 2.24 ms
+//   C4 (1024 poses, 512 tiles):  11473 / 11599 / 11760 / 11846 / 11895 / 12010
+//   C5 (16 poses, 8192 tiles):   492 / 494 / 493 / 483 / 477 / 477
+// DRR_POSE_GROUP > 0 fixes G (A/B builds).
+#ifndef DRR_POSE_GROUP
+#define DRR_POSE_GROUP 0
+#endif
+int pose_group(int n_poses, unsigned tiles) {
+  long G = DRR_POSE_GROUP > 0 ? DRR_POSE_GROUP : 16384L / (tiles > 0 ? tiles : 1);
+  return static_cast<int>(G < 1 ? 1 : (G > n_poses ? n_poses : G));
+}
+
+// The launch grid of a pose kernel; also sets d.pose_group for it.
+dim3 pose_grid(drr::DetDev& d, int n_poses, int K) {
   int tw, th;
   switch (K) {
     case 1: tw = drr::Tile<1>::W; th = drr::Tile<1>::H; break;
@@ -672,7 +704,9 @@ dim3 pose_grid(const drr::DetDev& d, int n_poses, int K) {
     case 4: tw = drr::Tile<4>::W; th = drr::Tile<4>::H; break;
     default: tw = drr::Tile<8>::W; th = drr::Tile<8>::H; break;
   }
-  return dim3((d.W + tw - 1) / tw, (d.H + th - 1) / th, n_poses);
+  const dim3 grd((d.W + tw - 1) / tw, (d.H + th - 1) / th, n_poses);
+  d.pose_group = pose_group(n_poses, grd.x * grd.y);
+  return grd;
 }
 
 // Dispatch a runtime K in {1, 2, 4, 8} to a template instantiation.
@@ -686,9 +720,10 @@ dim3 pose_grid(const drr::DetDev& d, int n_poses, int K) {
 
 template <typename VT, typename GT>
 void launch_backward(const VT* vol, const drr::GridDev& g,
-                            const double* frames, const drr::DetDev& d,
+                            const double* frames, const drr::DetDev& det,
                             int n_poses, const GT* grad, void* img,
                             int img_dtype, double* partials, cudaStream_t st) {
+  drr::DetDev d = det;
   const size_t smem = table_bytes(g, true);
   const int K = ray_split(d, n_poses);
   const dim3 grd = pose_grid(d, n_poses, K);
