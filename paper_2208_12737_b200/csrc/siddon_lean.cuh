@@ -63,7 +63,11 @@ constexpr int kLeanRecDoublesPerThread = 15;  // the largest record (gradient wa
 __host__ __device__ constexpr int lean_rec_doubles(bool grad_walk) {
   return grad_walk ? 15 : (DRR_LEAN_Q_FWD ? 14 : 9);
 }
-constexpr int kLeanThreads = 128;  // threads per CTA of every kernel using the walk
+constexpr int kLeanThreads = 128;
+#ifndef DRR_LEAN_UNROLL
+#define DRR_LEAN_UNROLL 1
+#endif
+constexpr int kLeanUnroll = DRR_LEAN_UNROLL;  // pipeline blocks per loop iteration  // threads per CTA of every kernel using the walk
 
 enum LeanMode { kLeanSum = 0, kLeanCount = 1, kLeanGrad = 2 };
 
@@ -346,6 +350,7 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     prev = cur;
   };
   const int n = r.count;
+#pragma unroll(kLeanUnroll)
   for (int blk = n / kLeanPipe; blk > 0; --blk) {
 #pragma unroll
     for (int j = 0; j < kLeanPipe; ++j) step(j);

@@ -499,3 +499,31 @@ def test_subnormal_direction_rays(cuda_device):
     sc = max(1.0, np.abs(rs).max(), np.abs(rp).max())
     np.testing.assert_allclose(gs, rs, atol=1e-10 * sc, rtol=0)
     np.testing.assert_allclose(gp, rp, atol=1e-10 * sc, rtol=0)
+
+
+def test_pose_group_order_is_invisible(cuda_device):
+    """The CTA order interleaves poses in groups of ~16K CTAs (drr_kernels.cu
+    pose_group): 40 poses on a 320x200 detector (550 tiles per pose) run as
+    groups of 29 + 11.  Images, ray Jacobians and frame gradients equal those
+    of one-pose launches bitwise; the forward-only kernel agrees too."""
+    from paper_2208_12737_b200 import (DeviceVolume, Detector, backward_from_jac, pose_frames,
+                                       render_frames, render_frames_jac, synthetic)
+    rng = np.random.default_rng(3)
+    vol = DeviceVolume(rng.uniform(0, 2, (40, 36, 30)).astype(np.float32), (1.5, 1.7, 2.0),
+                       device=cuda_device)
+    B, H, W = 40, 200, 320
+    det = Detector(H, W, 0.6, ray_split=1)
+    poses = synthetic.sample_poses((300.0, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0),
+                                   synthetic.NARROW_HALF_WIDTHS, B, seed=1)
+    frames = pose_frames(torch.tensor(poses, device=cuda_device), vol.center).detach()
+    g = torch.randn((B, H, W), device=cuda_device)
+    img, jac = render_frames_jac(vol, det, frames)
+    gf = backward_from_jac(det, jac, g)
+    assert torch.equal(render_frames(vol, det, frames), img)
+    assert float((img > 0).float().mean()) > 0.2  # the rays do cross the volume
+    jac = jac.view(6, B, H * W)
+    for b in range(B):
+        i1, j1 = render_frames_jac(vol, det, frames[b:b + 1].contiguous())
+        assert torch.equal(i1[0], img[b])
+        assert torch.equal(j1.view(6, H * W), jac[:, b])
+        assert torch.equal(backward_from_jac(det, j1, g[b:b + 1].contiguous())[0], gf[b])
