@@ -52,9 +52,11 @@ namespace drr {
 #endif
 // kQ record entry per axis: 1 = {table cursor, voxel byte step} in one 8-byte
 // word (one load; the table step, +-8, follows from the voxel step's sign);
+// 2 = the cursor and the voxel step as two 4-byte words, each contiguous over
+// the CTA's threads (one more load, but the cursor store is conflict-free);
 // 0 = {table step, voxel byte step} and the cursor in a separate word.
 #ifndef DRR_LEAN_QPACK
-#define DRR_LEAN_QPACK 1
+#define DRR_LEAN_QPACK 2
 #endif
 constexpr int kLeanRecDoublesPerThread = 15;  // the largest record (gradient walk)
 // Record doubles per thread a walk mode uses: {d, 1/d} x 3 and s x 3, plus
@@ -254,7 +256,15 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   const int db0 = db_init[0], db1 = db_init[1], db2 = db_init[2];
   int* sp = reinterpret_cast<int*>(rec + 9 * nt + threadIdx.x);
   uint32_t* qc = reinterpret_cast<uint32_t*>(rec + 12 * nt) + threadIdx.x;
-  if constexpr (kQ) {
+  // (QPACK 2) cursor words qw[a][tid], voxel steps qw[3 + a][tid]
+  uint32_t* qw = reinterpret_cast<uint32_t*>(rec + 9 * nt) + threadIdx.x;
+  if constexpr (kQ && DRR_LEAN_QPACK == 2) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      qw[a * nt] = qa_init[a];
+      qw[(3 + a) * nt] = static_cast<uint32_t>(db_init[a]);
+    }
+  } else if constexpr (kQ) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       sp[2 * a * nt] = DRR_LEAN_QPACK ? static_cast<int>(qa_init[a]) : 8 * r.st[a];
@@ -262,6 +272,8 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
       if (!DRR_LEAN_QPACK) qc[a * nt] = qa_init[a];
     }
   }
+  const uint32_t qw_s = static_cast<uint32_t>(__cvta_generic_to_shared(qw));
+  constexpr uint32_t qw_stride = 4u * nt;
   // (gradient walk) the end parameter and labels are only needed after the
   // loop: park them in the record instead of holding registers across it
   double* park_a = rec + 14 * nt + threadIdx.x;
@@ -307,7 +319,14 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     lds_2f64(dv_s + k * dv_stride, d, inv);
     double num;  // (o + k*sp) - s from the source-relative plane table
     int db;
-    if constexpr (kQ && DRR_LEAN_QPACK) {
+    if constexpr (kQ && DRR_LEAN_QPACK == 2) {
+      uint32_t qa;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(qa) : "r"(qw_s + k * qw_stride));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(db) : "r"(qw_s + (3 + k) * qw_stride));
+      num = lds_f64(qa);
+      const uint32_t qs = 8u + (static_cast<uint32_t>(db >> 31) << 4);  // +-8 by the walk's sign
+      asm volatile("st.shared.u32 [%0], %1;" :: "r"(qw_s + k * qw_stride), "r"(qa + qs) : "memory");
+    } else if constexpr (kQ && DRR_LEAN_QPACK) {
       uint32_t qa;  // {table cursor, voxel byte step}
       asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qa), "=r"(db)
                    : "r"(sp_s + k * sp_stride));
