@@ -35,13 +35,13 @@
 namespace drr {
 
 // Launch bounds (A/B on C2, 32 poses; scripts/gpu_ab.sh, gpu_ab_fast.sh): the
-// forward at 6 CTAs/SM with a 4-deep gather pipeline, k_forward_jac at 6 with
-// a 3-deep one (its derived-axis loop fits 80 registers once the walk's end
-// state is parked in shared memory and the direction re-read after it), the
-// re-walk k_backward at 5 (it spills at 6): 1.97 / 2.29 / 2.53 ms for 32
-// poses; ptxas spills only outside the walk's fast path.
+// forward at 6 CTAs/SM with a 4-deep gather pipeline, k_forward_jac and the
+// re-walk k_backward at 6 with a 3-deep one (their derived-axis loops fit 80
+// registers once the walk's end state is parked in shared memory and the
+// pixel and direction are re-derived after it; k_backward 2.34 -> 2.17 ms
+// going from 5 to 6); ptxas spills only outside the walk's fast path.
 #ifndef DRR_BWD_MINB
-#define DRR_BWD_MINB 5
+#define DRR_BWD_MINB 6
 #endif
 #ifndef DRR_FJ_MINB
 #define DRR_FJ_MINB 6
@@ -159,9 +159,9 @@ __device__ __forceinline__ void pixel_ray(const double* __restrict__ f,
 // across the walk loop instead: registers there are what bound occupancy).
 // Same operations as pixel_ray + ray_setup, so bit-identical.
 __device__ __forceinline__ void reload_ray_d(const double* __restrict__ f, const DetDev& det,
-                                             int h, int w, double* d) {
-  const double ah = (static_cast<double>(h) - det.half_h) * det.pitch_y;
-  const double aw = (static_cast<double>(w) - det.half_w) * det.pitch_x;
+                                             int h, int w, double* d, double& ah, double& aw) {
+  ah = (static_cast<double>(h) - det.half_h) * det.pitch_y;
+  aw = (static_cast<double>(w) - det.half_w) * det.pitch_x;
   double v[12];
 #pragma unroll
   for (int i = 0; i < 12; ++i)
@@ -310,16 +310,21 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
   }
 #pragma unroll
   for (int k = 0; k < 7; ++k) part[k] = chunk_sum<K>(part[k]);
-  if (valid && chunk == 0) {
-    const size_t pix = (static_cast<size_t>(b) * det.H + h) * det.W + w;
+  // the pixel and its ray again (volatile reads, as in k_forward_jac): nothing
+  // of them is held across the walk; d and L are chunk-invariant
+  tile_ray<K>(det, h, w, chunk);
+  const int bp = cta_pos(det).b;
+  if (h < det.H && w < det.W && chunk == 0) {
+    const size_t pix = (static_cast<size_t>(bp) * det.H + h) * det.W + w;
     const double gpx = static_cast<double>(grad_img[pix]);
-    // chunk 0's Ray holds the whole ray's direction (d, L are chunk-invariant)
-    const double L = ray_length(r);
+    double d[3];
+    reload_ray_d(frames + 12 * bp, det, h, w, d, ah, aw);
+    const double L = ray_length(d);
     const double e = L * part[0];
     if (part[0] != 0.0 || part[1] != 0.0 || part[2] != 0.0 || part[3] != 0.0 ||
         part[4] != 0.0 || part[5] != 0.0 || part[6] != 0.0) {
       double dEds[3], dEdp[3];
-      sums_to_endpoint_grads(r, part[0], part + 1, part + 4, L, dEds, dEdp);
+      sums_to_endpoint_grads(d, part[0], part + 1, part + 4, L, dEds, dEdp);
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         acc12[a] = gpx * dEds[a];
@@ -401,8 +406,8 @@ __global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
   const int bp = cta_pos(det).b;
   if (h < det.H && w < det.W && chunk == 0) {
     const size_t pix = (static_cast<size_t>(bp) * det.H + h) * det.W + w;
-    double d[3];
-    reload_ray_d(frames + 12 * bp, det, h, w, d);
+    double d[3], ah, aw;
+    reload_ray_d(frames + 12 * bp, det, h, w, d, ah, aw);
     const double L = ray_length(d);
     double dEds[3] = {0.0, 0.0, 0.0}, dEdp[3] = {0.0, 0.0, 0.0};
     if (part[0] != 0.0 || part[1] != 0.0 || part[2] != 0.0 || part[3] != 0.0 ||

@@ -6,7 +6,7 @@ cmd=[b.nvcc(),*b.NVCC_FLAGS,'-Xptxas=-v',*['-D'+d for d in defs],'-o','/tmp/x.so
 r=subprocess.run(cmd,capture_output=True,text=True)
 L=r.stderr.splitlines()
 for i,l in enumerate(L):
-    if 'Compiling entry' in l and ('IffLi1E' in l or 'IffLi8E' in l) and ('k_forward' in l):
+    if 'Compiling entry' in l and (('IffLi1E' in l or 'IffLi8E' in l) and 'k_forward' in l or 'k_backwardIfffLi1E' in l):
         nm=l.split("'")[1]
         nm=nm[5:30]
         j=i+1

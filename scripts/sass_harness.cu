@@ -7,3 +7,6 @@ template __global__ void drr::k_forward_jac<float, float, 1>(const float*, const
                                                              float*, double*, size_t);
 template __global__ void drr::k_forward<float, float, 1>(const float*, const drr::GridDev,
                                                          const double*, const drr::DetDev, float*);
+template __global__ void drr::k_backward<float, float, float, 1>(const float*, const drr::GridDev,
+                                                                 const double*, const drr::DetDev,
+                                                                 const float*, float*, double*);
