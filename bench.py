@@ -389,7 +389,7 @@ def main():
             "bj": lambda: backward_from_jac(drr.detector, jac_holder["jac"], g_img),
             "fwd": lambda: render_frames(drr.volume, drr.detector, frames),
             "rewalk": lambda: backward_frames(drr.volume, drr.detector, frames, g_img)}
-    for i in range(8):
+    for i in range(12):
         for name in ("fj", "bj", "fwd", "rewalk"):
             flush.fill_(1.0)
             e0 = torch.cuda.Event(enable_timing=True)
@@ -400,7 +400,7 @@ def main():
             e1.synchronize()
             if i >= 2:
                 kt[name].append(e0.elapsed_time(e1))
-    kms = {k: float(np.mean(v)) for k, v in kt.items()}
+    kms = {k: float(np.mean(v)) for k, v in kt.items()}  # average launch duration, 10 launches
     fj_ms = kms["fj"]
     # algorithmic bytes per k_forward_jac launch: one fp32 gather per used
     # voxel-step + fp32 image store + 6 f64 Jacobian entries per pixel
