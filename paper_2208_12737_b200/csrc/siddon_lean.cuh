@@ -31,10 +31,10 @@ namespace drr {
 // (conflict-free LDS.128).  The plane table is source-relative
 // (build_plane_table), so a voxel-step reads {d, 1/d} and the numerator.
 // Walk tuning, per mode (A/B on C2, see profiles/):
-//  * kQ: the record also holds each axis's plane-table cursor and its strides
-//    ({1/d, table step, voxel byte step} 16 B, cursor 4 B), so the winner's
-//    bookkeeping is one record load and one store instead of per-axis selects
-//    (fewer ALU/issue slots, more shared-memory wavefronts);
+//  * kQ: the record also holds each axis's plane-table cursor and voxel byte
+//    step, so the winner's bookkeeping is two record loads and one store
+//    instead of per-axis selects (fewer ALU/issue slots, more shared-memory
+//    wavefronts): the gradient walks use it, the forward does not;
 //  * PD: gather pipeline depth -- a segment's voxel value is consumed PD steps
 //    after its load is issued (ncu lean1: 45% of stall samples waited on the
 //    gather when it was consumed one step later).
@@ -50,26 +50,23 @@ namespace drr {
 #ifndef DRR_LEAN_Q_GRAD
 #define DRR_LEAN_Q_GRAD 1
 #endif
-// kQ record entry per axis: 1 = {table cursor, voxel byte step} in one 8-byte
-// word (one load; the table step, +-8, follows from the voxel step's sign);
-// 2 = the cursor and the voxel step as two 4-byte words, each contiguous over
-// the CTA's threads (one more load, but the cursor store is conflict-free);
-// 0 = {table step, voxel byte step} and the cursor in a separate word.
-#ifndef DRR_LEAN_QPACK
-#define DRR_LEAN_QPACK 2
-#endif
+// kQ record words per axis: the table cursor and the voxel byte step, each
+// contiguous over the CTA's threads (qw below); the table step (+-8) follows
+// from the voxel step's sign.  A/B on C2 fwd+jac: 2.08 ms, vs 2.14 for one
+// 8-byte {cursor, step} word per thread (its cursor store is 8-byte strided:
+// bank conflicts) and 2.16 for {table step, voxel step} beside the cursor.
 constexpr int kLeanRecDoublesPerThread = 15;  // the largest record (gradient walk)
 // Record doubles per thread a walk mode uses: {d, 1/d} x 3 and s x 3, plus
-// (kQ) the table / voxel steps and the 3 table cursors, plus (gradient walk)
-// the walk's end parameter and labels, parked there for the loop's duration.
+// (kQ) the cursor and voxel-step words, plus (gradient walk) the walk's end
+// parameter and labels, parked there for the loop's duration.
 __host__ __device__ constexpr int lean_rec_doubles(bool grad_walk) {
   return grad_walk ? 15 : (DRR_LEAN_Q_FWD ? 14 : 9);
 }
-constexpr int kLeanThreads = 128;
+constexpr int kLeanThreads = 128;  // threads per CTA of every kernel using the walk
 #ifndef DRR_LEAN_UNROLL
 #define DRR_LEAN_UNROLL 1
 #endif
-constexpr int kLeanUnroll = DRR_LEAN_UNROLL;  // pipeline blocks per loop iteration  // threads per CTA of every kernel using the walk
+constexpr int kLeanUnroll = DRR_LEAN_UNROLL;  // pipeline blocks per loop iteration
 
 enum LeanMode { kLeanSum = 0, kLeanCount = 1, kLeanGrad = 2 };
 
@@ -234,10 +231,11 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   // voxel bookkeeping as a byte pointer (a certified segment's voxel is in
   // range: its midpoint is more than the rounding noise inside every slab)
   const char* bp = reinterpret_cast<const char*>(vol + r.flat);
-  // record layout (structure of arrays over the CTA's threads):
-  //   dv[a][tid] = {d_a, 1/d_a} (the winner's division constants: one
-  //   LDS.128); sv[a][tid] = s_a (exact path only); (kQ) sp[a][tid] =
-  //   {table step, voxel byte step}, qc[a][tid] = table cursor
+  // record layout (structure of arrays over the CTA's threads, in doubles
+  // of nt): dv[a][tid] = {d_a, 1/d_a} (the winner's division constants: one
+  // LDS.128) at 0; sv[a][tid] = s_a (exact path only) at 6; (kQ) qw[a][tid]
+  // = table cursor, qw[3 + a][tid] = voxel byte step (4-byte words) at 9;
+  // (gradient walk) the parked exit labels at 13.5 and end parameter at 14
   constexpr int nt = kLeanThreads;
   double* dv = rec + 2 * threadIdx.x;
   double* sv = rec + 6 * nt + threadIdx.x;
@@ -254,22 +252,12 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   uint32_t qa0 = qa_init[0], qa1 = qa_init[1], qa2 = qa_init[2];
   const int qs0 = 8 * r.st[0], qs1 = 8 * r.st[1], qs2 = 8 * r.st[2];
   const int db0 = db_init[0], db1 = db_init[1], db2 = db_init[2];
-  int* sp = reinterpret_cast<int*>(rec + 9 * nt + threadIdx.x);
-  uint32_t* qc = reinterpret_cast<uint32_t*>(rec + 12 * nt) + threadIdx.x;
-  // (QPACK 2) cursor words qw[a][tid], voxel steps qw[3 + a][tid]
   uint32_t* qw = reinterpret_cast<uint32_t*>(rec + 9 * nt) + threadIdx.x;
-  if constexpr (kQ && DRR_LEAN_QPACK == 2) {
+  if constexpr (kQ) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       qw[a * nt] = qa_init[a];
       qw[(3 + a) * nt] = static_cast<uint32_t>(db_init[a]);
-    }
-  } else if constexpr (kQ) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      sp[2 * a * nt] = DRR_LEAN_QPACK ? static_cast<int>(qa_init[a]) : 8 * r.st[a];
-      sp[2 * a * nt + 1] = db_init[a];
-      if (!DRR_LEAN_QPACK) qc[a * nt] = qa_init[a];
     }
   }
   const uint32_t qw_s = static_cast<uint32_t>(__cvta_generic_to_shared(qw));
@@ -277,14 +265,11 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
   // (gradient walk) the end parameter and labels are only needed after the
   // loop: park them in the record instead of holding registers across it
   double* park_a = rec + 14 * nt + threadIdx.x;
-  uint32_t* park_l = qc + 3 * nt;
+  uint32_t* park_l = reinterpret_cast<uint32_t*>(rec + 12 * nt) + 3 * nt + threadIdx.x;
   if constexpr (kMode == kLeanGrad) {
     *park_a = r.amax;
     *park_l = static_cast<uint32_t>(r.lab_max) | (static_cast<uint32_t>(r.D) << 8);
   }
-  const uint32_t sp_s = static_cast<uint32_t>(__cvta_generic_to_shared(sp));
-  const uint32_t qc_s = static_cast<uint32_t>(__cvta_generic_to_shared(qc));
-  constexpr uint32_t sp_stride = 8u * nt, qc_stride = 4u * nt;
   asm volatile("" ::: "memory");  // the record stores precede every record load
   const double T2 = fmax(r.T, kSegEps);
   double prev = r.amin;
@@ -319,28 +304,13 @@ __device__ __forceinline__ void lean_walk_impl(const VT* __restrict__ vol, const
     lds_2f64(dv_s + k * dv_stride, d, inv);
     double num;  // (o + k*sp) - s from the source-relative plane table
     int db;
-    if constexpr (kQ && DRR_LEAN_QPACK == 2) {
+    if constexpr (kQ) {
       uint32_t qa;
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(qa) : "r"(qw_s + k * qw_stride));
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(db) : "r"(qw_s + (3 + k) * qw_stride));
       num = lds_f64(qa);
       const uint32_t qs = 8u + (static_cast<uint32_t>(db >> 31) << 4);  // +-8 by the walk's sign
       asm volatile("st.shared.u32 [%0], %1;" :: "r"(qw_s + k * qw_stride), "r"(qa + qs) : "memory");
-    } else if constexpr (kQ && DRR_LEAN_QPACK) {
-      uint32_t qa;  // {table cursor, voxel byte step}
-      asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qa), "=r"(db)
-                   : "r"(sp_s + k * sp_stride));
-      num = lds_f64(qa);
-      const uint32_t qs = 8u + (static_cast<uint32_t>(db >> 31) << 4);  // +-8 by the walk's sign
-      asm volatile("st.shared.u32 [%0], %1;" :: "r"(sp_s + k * sp_stride), "r"(qa + qs) : "memory");
-    } else if constexpr (kQ) {
-      int qs;  // {table step, voxel byte step}
-      asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qs), "=r"(db)
-                   : "r"(sp_s + k * sp_stride));
-      uint32_t qa;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(qa) : "r"(qc_s + k * qc_stride));
-      num = lds_f64(qa);
-      asm volatile("st.shared.u32 [%0], %1;" :: "r"(qc_s + k * qc_stride), "r"(qa + qs) : "memory");
     } else {
       num = lds_f64(m0 * qa0 + m1 * qa1 + m2 * qa2);
       qa0 += m0 * qs0;
