@@ -414,11 +414,13 @@ def main():
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     traffic = None  # dram bytes per k_forward_jac launch from the committed ncu capture
+    limiter = None  # what ncu shows binding that kernel (it is not HBM)
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)["k_forward_jac"]
         if tr.get("poses") == B and tr.get("config") == "C2":
             traffic = float(tr["traffic_bytes_per_launch"])
+            limiter = tr.get("limiter")
     except (OSError, KeyError, ValueError):
         pass
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
@@ -476,7 +478,7 @@ def main():
                      "achieved": achieved_fj, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved_fj / hbm_peak, "traffic": traffic,
                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same kernel/config)",
-                     "peak_source": peak_src,
+                     "peak_source": peak_src, "limiter": limiter,
                      "algorithmic_bytes_per_launch": bytes_fj, "launch_ms": fj_ms},
         "kernels": {"forward_jac_ms": fj_ms, "backward_jac_ms": kms["bj"],
                     "forward_only_ms": kms["fwd"], "rewalk_backward_ms": kms["rewalk"],
