@@ -673,12 +673,16 @@ int make_det(const drr_detector* in, drr::DetDev& d) {
 }
 
 // Threads per ray: explicit, or auto = the smallest K in {1, 2, 4, 8} with
-// B*H*W*K >= ~2 resident waves of threads (148 SMs x 1024 x 2).
+// B*H*W*K >= one wave of resident threads (148 SMs x 6 CTAs x 128).  A/B
+// (scripts/kbench_split.py, one pose, fwd+jac+contraction / forward ms for
+// K = 1 / 2 / 4 / 8): C2 200^2 0.218 / 0.150 / 0.147 / 0.161 and 0.171 /
+// 0.114 / 0.112 / 0.124 (K = 4 chosen; two waves would pick 8); C1 100^2
+// forward 0.057 / 0.047 / 0.039 / 0.034 (K = 8).
 int ray_split(const drr::DetDev& d, int n_poses) {
   if (d.split > 0) return d.split;
   const double rays = static_cast<double>(n_poses) * d.H * d.W;
   int k = 1;
-  while (k < 8 && rays * k < 148.0 * 1024.0 * 2.0) k *= 2;
+  while (k < 8 && rays * k < 148.0 * 6.0 * 128.0) k *= 2;
   return k;
 }
 
