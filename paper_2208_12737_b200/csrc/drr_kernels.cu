@@ -1042,18 +1042,30 @@ int drr_image_loss(const void* d_img, const void* d_fixed, int img_dtype, int64_
   if (fixed_stride != 0 && fixed_stride != npix)
     return fail(DRR_ERR_INVALID_ARGUMENT, "fixed_stride must be 0 or npix");
   if (n_images == 0) return DRR_OK;
-  const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (img_dtype == 0)
-    drr::k_image_loss<float><<<n_images, drr::kLossThreads, 0, st>>>(
-        static_cast<const float*>(d_img), static_cast<const float*>(d_fixed), fixed_stride, npix,
-        kind, d_value, d_grad, d_status);
-  else if (img_dtype == 1)
-    drr::k_image_loss<double><<<n_images, drr::kLossThreads, 0, st>>>(
-        static_cast<const double*>(d_img), static_cast<const double*>(d_fixed), fixed_stride,
-        npix, kind, d_value, d_grad, d_status);
-  else
+  if (img_dtype != 0 && img_dtype != 1)
     return fail(DRR_ERR_INVALID_ARGUMENT, "unknown img_dtype %d", img_dtype);
-  return check_launch("drr_image_loss");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // one cluster per image: grid (kLossCluster, images), images in launches of
+  // at most 65535 (the grid's y limit)
+  for (int32_t i0 = 0; i0 < n_images; i0 += 65535) {
+    const int32_t n = n_images - i0 < 65535 ? n_images - i0 : 65535;
+    const dim3 grd(drr::kLossCluster, n);
+    const int64_t fo = fixed_stride * i0, io = npix * i0;
+    double* val = d_value + i0;
+    float* grad = d_grad ? d_grad + io : nullptr;
+    int* sts = d_status ? d_status + i0 : nullptr;
+    if (img_dtype == 0)
+      drr::k_image_loss<float><<<grd, drr::kLossThreads, 0, st>>>(
+          static_cast<const float*>(d_img) + io, static_cast<const float*>(d_fixed) + fo,
+          fixed_stride, npix, kind, val, grad, sts);
+    else
+      drr::k_image_loss<double><<<grd, drr::kLossThreads, 0, st>>>(
+          static_cast<const double*>(d_img) + io, static_cast<const double*>(d_fixed) + fo,
+          fixed_stride, npix, kind, val, grad, sts);
+    const int rc = check_launch("drr_image_loss");
+    if (rc) return rc;
+  }
+  return DRR_OK;
 }
 
 int drr_register_update(double* d_eta, double* d_velocity, const double* d_grad_frames,
