@@ -22,7 +22,12 @@
 
 namespace drr {
 
-constexpr int kLossThreads = 256;
+// threads per CTA (A/B, scripts/lossbench.py, 1 / 32 images of 200^2: 128 -> 11.5 / 12.8 us,
+// 256 -> 11.3 / 11.1, 512 -> 11.5 / 11.4, 1024 -> 11.2 / 20.7)
+#ifndef DRR_LOSS_THREADS
+#define DRR_LOSS_THREADS 256
+#endif
+constexpr int kLossThreads = DRR_LOSS_THREADS;
 constexpr int kLossCluster = 8;  // CTAs (SMs) per image
 constexpr int kLossBatch = 4;    // loads in flight per thread before they are summed (in order)
 
