@@ -171,3 +171,31 @@ def test_module_losses_fused_match_torch(cuda_device):
                                        rtol=1e-12, atol=1e-12)
             gx, gy = x.grad.double().cpu().numpy(), y.grad.cpu().numpy()
             np.testing.assert_allclose(gx, gy, rtol=1e-6, atol=1e-6 * np.abs(gy).max())
+
+
+def test_image_loss_cluster_edge_sizes(cuda_device):
+    """The loss kernel splits each image over an 8-CTA cluster: images with
+    fewer pixels than CTAs (empty chunks), and large ones (several batched
+    load rounds per thread) match the oracle, and two calls agree bitwise."""
+    _l, lib = _lib()
+    rng = np.random.default_rng(9)
+    for B, H, W in ((2, 1, 5), (1, 3, 3), (2, 300, 310)):
+        a = rng.random((B, H, W)) * 50
+        b = rng.random((B, H, W)) * 20 + 0.5 * a
+        at = torch.tensor(a, dtype=torch.float64, device=cuda_device)
+        bt = torch.tensor(b, dtype=torch.float64, device=cuda_device)
+        outs = []
+        for _ in range(2):
+            val = torch.empty(B, dtype=torch.float64, device=cuda_device)
+            grad = torch.empty((B, H, W), dtype=torch.float32, device=cuda_device)
+            _l.check(lib.drr_image_loss(at.data_ptr(), bt.data_ptr(), 1, H * W, B, H * W,
+                                        _l.DRR_LOSS_NEG_ZNCC, val.data_ptr(), grad.data_ptr(),
+                                        None, torch.cuda.current_stream().cuda_stream))
+            outs.append((val.clone(), grad.clone()))
+        assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+        val, grad = outs[0]
+        for i in range(B):
+            rv, rg = O.neg_zncc_value_and_grad(a[i], b[i])
+            assert float(val[i]) == pytest.approx(rv, abs=1e-12)
+            np.testing.assert_allclose(grad[i].cpu().numpy(), rg, rtol=1e-5,
+                                       atol=1e-6 * np.abs(rg).max())
