@@ -1,20 +1,24 @@
 #!/usr/bin/env python
 """Benchmark: DRRs/sec fwd+bwd (200x200 detector, 512x512x133 CT) on B200.
 
-One STEP = the hot path over one batch of poses: for B poses per GPU, render
-the 200x200 DRRs with each ray's Jacobian (drr_forward_jac: one CT walk),
-evaluate the reference's registration loss (neg-ZNCC vs a fixed DRR,
-metrics.py:71-91) and back-propagate to the pose (drr_backward_jac + the
-12-number frame chain) -- i.e. B x the
-reference's ``loss_and_gradient`` (gradients.py:61-69), config C2 of
-SURVEY.md 8(d) with the C4 pose sampling.  Poses shard across ranks with no
-collective in the loop (weak scaling); the CT is NCCL-broadcast once.
+One STEP = the hot path over one fixed global batch of poses (default 256):
+for every pose, render the 200x200 DRR, evaluate the reference's registration
+loss (neg-ZNCC vs a fixed DRR, metrics.py:71-91) and back-propagate to the
+pose -- the reference's ``loss_and_gradient`` (gradients.py:61-69) for each
+pose, config C2 of SURVEY.md 8(d) with the C4 pose sampling.  On N GPUs the
+batch is sharded over the ranks (strong scaling: the work per step is fixed):
+each rank walks its block of poses and its kernels store the per-pose loss and
+7-gradient straight into rank 0's buffers over NVLink
+(distributed.ShardedDRR); the CT is NCCL-broadcast once before timing.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
 
 Prints ONE JSON line (rank 0).  Timing: CUDA events per step on the launching
 stream, L2 flushed (256 MiB write) between timed steps outside the events,
-max over ranks.
+max over ranks.  Also measured (rank 0's line, keys below): the same step
+end to end (pinned host poses in, loss + gradient back on the host), the C1 /
+C4 / C5 configs, C3 registration, the dominant kernel against the HBM
+roofline, and the reference's CPU path on this host.
 """
 
 from __future__ import annotations
@@ -39,10 +43,12 @@ H = W = 200
 PITCH = 3.6
 RHO = 300.0
 TRUTH = (RHO, math.pi / 2, math.pi / 2, 0.0, 0.0, 0.0, 0.0)
+METRIC = "DRRs/sec fwd+bwd (200x200 det, 512x512x133 CT)"
 WORKLOAD = ("C2: synthetic chest CT 512x512x133 @ (0.703125,0.703125,2.5) mm fp32, "
-            "200x200 detector @ 3.6 mm, rho=sdr=300 mm; per step B poses (narrow samples "
-            "around AP, seed 0) x [forward DRR + neg-ZNCC vs fixed DRR + backward to "
-            "(rotation, translation)]")
+            "200x200 detector @ 3.6 mm, rho=sdr=300 mm; per step a fixed global batch of poses "
+            "(narrow samples around AP, seed 0) x [forward DRR + neg-ZNCC vs fixed DRR at the "
+            "truth pose + backward to (rho, rotation, translation)], sharded over the GPUs, "
+            "per-pose loss and gradient collected on rank 0")
 
 
 def parse():
@@ -50,12 +56,13 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--batch", type=int, default=32, help="poses per GPU per step")
+    p.add_argument("--batch", type=int, default=256, help="global poses per step (all GPUs)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-other-configs", action="store_true",
-                   help="skip the C1/C4/C5 context measurements")
-    p.add_argument("--cpu-sample", type=int, default=0, help="poses for the CPU baseline (0: auto)")
+                   help="skip the C1/C3/C4/C5 context measurements")
+    p.add_argument("--cpu-seconds", type=float, default=15.0,
+                   help="wall-time budget of the CPU-baseline sample")
     return p.parse_args()
 
 
@@ -75,7 +82,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             time.sleep(0.5)  # nvidia-smi start-up: sample before the timed region begins
         except OSError:
@@ -113,37 +120,36 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baseline
-def _ref_worker(args):
-    """One pose of the reference's loss_and_gradient (native backend, 1 core)."""
-    eta, fixed = args
-    from oracle.oracle import reference_module
-    dt = reference_module()
-    vol = _REF_STATE["vol"]
-    spec = _REF_STATE["spec"]
-    t0 = time.perf_counter()
-    rec = dt.loss_and_gradient(vol, dt.PoseParameters.from_vector(eta), spec, fixed,
-                               "neg_zncc", backend="native")
-    return time.perf_counter() - t0, float(rec.value)
-
-
+# The reference's own CPU path: drrtrace's loss_and_gradient with its native
+# (Cython, single-threaded, GIL-holding) backend from oracle/_ref, one pose per
+# call, pose-sharded over a fork pool created ONCE (outside any timed region).
 _REF_STATE = {}
 
 
-def _port_worker(args):
+def _ref_worker(eta):
+    from oracle.oracle import reference_module
+    dt = reference_module()
+    st = _REF_STATE
+    t0 = time.perf_counter()
+    rec = dt.loss_and_gradient(st["vol"], dt.PoseParameters.from_vector(eta), st["spec"],
+                               st["fixed"], "neg_zncc", backend="native")
+    return time.perf_counter() - t0, float(rec.value)
+
+
+def _port_worker(eta):
     """Fallback when oracle/_ref is absent: the C oracle (port) fwd + bwd."""
-    eta, fixed = args
     from oracle import oracle as O
     st = _REF_STATE
     t0 = time.perf_counter()
     frame = O.pose_frame(eta, st["center"])
     img = O.render(st["flat"], DIMS, SPACING, (0, 0, 0), frame, H, W, PITCH, PITCH)
-    _, pg = O.neg_zncc_value_and_grad(img, fixed)
+    val, pg = O.neg_zncc_value_and_grad(img, st["fixed"])
     O.render_backward(st["flat"], DIMS, SPACING, (0, 0, 0), frame, H, W, PITCH, PITCH, pg)
-    return time.perf_counter() - t0, 0.0
+    return time.perf_counter() - t0, float(val)
 
 
 def cpu_setup(vol_np):
-    """Reference inputs: the fp32 CT cast back to f64."""
+    """Reference inputs: the fp32 CT cast back to f64 (the GPU arm's values)."""
     from oracle.oracle import reference_module
     dt = reference_module()
     flat = vol_np.astype(np.float64).ravel(order="F")
@@ -151,25 +157,44 @@ def cpu_setup(vol_np):
     _REF_STATE.update(flat=flat, center=center)
     if dt is not None:
         vol = dt.Volume(DIMS, SPACING, (0.0, 0.0, 0.0), vol_np.astype(np.float64))
-        _REF_STATE.update(vol=vol, spec=dt.DetectorSpec.for_volume(vol, H, W, (PITCH, PITCH)))
-        fixed = dt.render(vol, dt.PoseParameters.from_vector(TRUTH), _REF_STATE["spec"]).values
-        return "reference", _ref_worker, fixed
+        spec = dt.DetectorSpec.for_volume(vol, H, W, (PITCH, PITCH))
+        fixed = dt.render(vol, dt.PoseParameters.from_vector(TRUTH), spec).values
+        _REF_STATE.update(vol=vol, spec=spec, fixed=fixed)
+        return "reference", _ref_worker
     from oracle import oracle as O
     frame = O.pose_frame(np.asarray(TRUTH), center)
-    fixed = O.render(flat, DIMS, SPACING, (0, 0, 0), frame, H, W, PITCH, PITCH)
-    return "port", _port_worker, fixed
+    _REF_STATE.update(fixed=O.render(flat, DIMS, SPACING, (0, 0, 0), frame, H, W, PITCH, PITCH))
+    return "port", _port_worker
 
 
-def cpu_run(worker, poses, fixed, procs):
-    """Pose-sharded fork pool (the reference kernels hold the GIL)."""
-    import multiprocessing as mp
-    t0 = time.perf_counter()
-    if procs <= 1:
-        res = [worker((p, fixed)) for p in poses]
-    else:
-        with mp.get_context("fork").Pool(procs) as pool:
-            res = pool.map(worker, [(p, fixed) for p in poses], chunksize=1)
-    return time.perf_counter() - t0, res
+class CpuPool:
+    """Fork pool of `procs` reference processes, created once."""
+
+    def __init__(self, worker, procs):
+        import multiprocessing as mp
+        self.worker, self.procs = worker, procs
+        self.pool = mp.get_context("fork").Pool(procs) if procs > 1 else None
+        if self.pool is not None:  # import the reference in every worker before timing
+            self.pool.map(_noop, range(procs), chunksize=1)
+
+    def run(self, poses):
+        t0 = time.perf_counter()
+        if self.pool is None:
+            res = [self.worker(p) for p in poses]
+        else:
+            res = self.pool.map(self.worker, list(poses), chunksize=1)
+        return time.perf_counter() - t0, res
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
+
+
+def _noop(_):
+    from oracle.oracle import reference_module
+    reference_module()
+    return 0
 
 
 def cpu_model():
@@ -183,143 +208,36 @@ def cpu_model():
     return "unknown"
 
 
-# ------------------------------------------------------------------- main
-# ------------------------------------------------- the other BASELINE configs
-def other_configs(dev, vol_c2, timed_fn, flush):
-    """C1 / C4 / C5 of BASELINE.json measured on this GPU (rank 0, N=1; they are
-    parity-test cases in tests/test_gpu_configs.py, reported here for context,
-    not the headline).  Device time with CUDA events, L2 flushed between reps."""
-    import torch
-    from paper_2208_12737_b200 import (DeviceVolume, Detector, backward_from_jac, count_steps,
-                                       pose_frames, render_frames, render_frames_jac, synthetic)
-    out = {}
-    # C1: 128^3 sphere @ 1 mm, 100^2 @ 2.56 mm, one oblique pose, forward only
-    v1 = DeviceVolume(synthetic.make_phantom("sphere", 128, 1.0), 1.0, device=dev)
-    d1 = Detector(100, 100, 2.56)
-    f1 = pose_frames(torch.tensor([[300.0, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0]], device=dev),
-                     v1.center).detach()
-    t = timed_fn(lambda: render_frames(v1, d1, f1), 20, 3)
-    out["C1"] = {"workload": "128^3 sphere @1 mm, 100x100 @2.56 mm, 1 pose, forward",
-                 "ms_per_drr": float(np.median(t))}
-    # C4: C2 volume, 1024 narrow poses (seed 0), 256^2 @ 2.8125 mm, forward only
-    d4 = Detector(256, 256, 2.8125)
-    p4 = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, 1024, seed=0)
-    f4 = pose_frames(torch.tensor(p4, device=dev), vol_c2.center).detach()
-    t = timed_fn(lambda: render_frames(vol_c2, d4, f4), 5, 2)
-    S4 = float(count_steps(vol_c2, d4, f4[:128].contiguous()).double().sum()) / 128
-    out["C4"] = {"workload": "C2 volume, 1024 narrow poses seed 0, 256x256 @2.8125 mm, forward, "
-                             "one launch (per-GPU shard at N=1)",
-                 "ms_per_batch": float(np.median(t)), "drr_per_s": 1024 / (float(np.median(t)) / 1e3),
-                 "voxel_steps_per_drr": S4}
-    # C5: 512^3 @ 0.703125 (sphere + 3x off-centre cube + noise), 1024^2 @ 0.703125,
-    # forward + backward; 16 poses per launch (the Jacobian of 16 poses is 0.8 GB)
-    n = 512
-    c = (torch.arange(n, device=dev, dtype=torch.float64) + 0.5) * 0.703125
-    mid, rad = n * 0.703125 / 2, 0.4 * n * 0.703125
-    r2 = (c - mid)[:, None, None] ** 2 + (c - mid)[None, :, None] ** 2 + (c - mid)[None, None, :] ** 2
-    frac = (torch.arange(n, device=dev, dtype=torch.float64) + 0.5) / n
-    inb = (frac >= 0.25) & (frac <= 0.5)
-    v5 = (r2 <= rad * rad).double() + 3.0 * (inb[:, None, None] & inb[None, :, None] & inb[None, None, :]).double()
-    gen = torch.Generator(device=dev).manual_seed(5)
-    v5 = torch.clamp(v5 + 0.01 * torch.randn(v5.shape, device=dev, generator=gen, dtype=torch.float64)
-                     * (v5 > 0), min=0.0).float()
-    vol5 = DeviceVolume(v5, 0.703125, device=dev)
-    del v5, r2
-    d5 = Detector(1024, 1024, 0.703125)
-    p5 = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, 16, seed=0)
-    f5 = pose_frames(torch.tensor(p5, device=dev), vol5.center).detach()
-    g5 = torch.randn((16, 1024, 1024), device=dev)
-    hold = {}
-
-    def c5_step():
-        hold["img"], hold["jac"] = render_frames_jac(vol5, d5, f5)
-        backward_from_jac(d5, hold["jac"], g5)
-
-    t = timed_fn(c5_step, 3, 1)
-    out["C5"] = {"workload": "512^3 @0.703125 sphere+3x cube+noise, 1024x1024 @0.703125, "
-                             "16 poses per launch, forward + backward (one walk + contraction)",
-                 "ms_per_batch": float(np.median(t)), "drr_per_s": 16 / (float(np.median(t)) / 1e3)}
-    del vol5, hold
-    torch.cuda.empty_cache()
-    return out
-
-
-def main():
-    args = parse()
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-
+def cpu_baseline(poses, budget_s):
+    """The reference on this host: 1 process on 1 core, then os.cpu_count()
+    processes (pose-sharded), on the GPU arm's own poses."""
     from paper_2208_12737_b200 import synthetic
+    kind, worker = cpu_setup(synthetic.chest_phantom(DIMS))
+    procs = os.cpu_count() or 1
+    t1 = []
+    t_start = time.perf_counter()
+    i = 0
+    while i < 2 or (time.perf_counter() - t_start < 0.2 * budget_s and i < 8):
+        t1.append(worker(poses[i % len(poses)])[0])
+        i += 1
+    one_core = 1.0 / float(np.median(t1))
+    pool = CpuPool(worker, procs)
+    n = procs * max(1, int(0.8 * budget_s * one_core))
+    n = min(n, procs * 64)
+    wall, res = pool.run([poses[j % len(poses)] for j in range(n)])
+    pool.close()
+    return {
+        "value": n / wall, "unit": "DRR/s", "cores": procs, "kind": kind,
+        "one_core": {"value": one_core, "unit": "DRR/s", "cores": 1,
+                     "sample": f"{len(t1)} poses, one at a time in this process"},
+        "sample": f"{n} poses of the GPU arm's C2 batch (loss_and_gradient, neg-ZNCC, native "
+                  f"backend, f64), pose-sharded over a {procs}-process fork pool created "
+                  f"before timing; {wall:.1f} s wall; CPU {cpu_model()}"}
 
-    if args.impl == "reference":
-        if rank != 0:
-            return 0
-        return run_reference(args, world)
 
+# ------------------------------------------------------------- GPU helpers
+def make_timer(dev, flush):
     import torch
-    import torch.distributed as dist
-    from paper_2208_12737_b200 import (DRR, backward_frames, backward_from_jac, count_steps,
-                                       pose_frames, render_frames, render_frames_jac)
-
-    from paper_2208_12737_b200 import _lib
-    from paper_2208_12737_b200.metrics import neg_zncc
-
-    # DRR_BENCH_SHARED_GPU=1 (testing only) puts every rank on cuda:0 with the
-    # gloo backend, so the multi-rank path can be exercised on a one-GPU box.
-    shared = os.environ.get("DRR_BENCH_SHARED_GPU") == "1"
-    dev = torch.device("cuda", 0 if shared else local)
-    torch.cuda.set_device(dev)
-    if world > 1:
-        if shared:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
-
-    # --- volume: built on rank 0, NCCL-broadcast once (SURVEY 5) --------
-    if rank == 0:
-        vol_np = synthetic.chest_phantom(DIMS)
-        vol_t = torch.from_numpy(vol_np).to(dev)
-    else:
-        vol_np = None
-        vol_t = torch.empty(DIMS, dtype=torch.float32, device=dev)
-    if world > 1:
-        dist.broadcast(vol_t, src=0)
-    drr = DRR(vol_t, SPACING, sdr=RHO, height=H, delx=PITCH, device=dev, strict=False)
-    del vol_t
-
-    # --- poses: global batch sharded by rank, no comms in the loop -------
-    B = args.batch
-    all_poses = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, B * world, seed=0)
-    poses_np = all_poses[rank * B:(rank + 1) * B]
-    rot0 = torch.tensor(poses_np[:, 1:4], device=dev)
-    tra0 = torch.tensor(poses_np[:, 4:7], device=dev)
-    with torch.no_grad():
-        fixed = drr(torch.tensor(TRUTH[1:4], device=dev), torch.tensor(TRUTH[4:7], device=dev))
-    fixed_b = fixed.expand(B, H, W)
-
-    from paper_2208_12737_b200.registration import _Buffers, loss_and_gradient
-
-    eta0 = torch.tensor(poses_np, device=dev)
-    bufs = _Buffers(drr.volume, drr.detector, B)
-
-    def step(eta):
-        # the reference's unit of work, batched: loss_and_gradient
-        # (gradients.py:61-69) = pose frames -> forward -> fused neg-ZNCC + pixel
-        # gradient -> Jacobian contraction (+ fixed-order reduce) -> pose gradient
-        # (6 native launches; the CT is walked once per ray)
-        return loss_and_gradient(drr.volume, drr.detector, eta, fixed, "neg_zncc", buffers=bufs)
-
-    def module_step(rot, tra):
-        # the north-star nn.Module path (torch autograd around drr_forward_jac /
-        # drr_backward_jac)
-        rot = rot.detach().requires_grad_(True)
-        tra = tra.detach().requires_grad_(True)
-        loss = neg_zncc(drr(rot, tra), fixed_b)
-        loss.sum().backward()
-        return loss.detach(), rot.grad, tra.grad
-
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def timed(fn, n, warm):
@@ -335,77 +253,233 @@ def main():
             if i >= warm:
                 out.append(e0.elapsed_time(e1))
         return out
+    return timed
+
+
+def c5_volume(dev):
+    """512^3 @ 0.703125 (sphere + 3x off-centre cube + noise), SURVEY 8(d) C5."""
+    import torch
+    n = 512
+    c = (torch.arange(n, device=dev, dtype=torch.float64) + 0.5) * 0.703125
+    mid, rad = n * 0.703125 / 2, 0.4 * n * 0.703125
+    r2 = (c - mid)[:, None, None] ** 2 + (c - mid)[None, :, None] ** 2 + (c - mid)[None, None, :] ** 2
+    frac = (torch.arange(n, device=dev, dtype=torch.float64) + 0.5) / n
+    inb = (frac >= 0.25) & (frac <= 0.5)
+    v5 = (r2 <= rad * rad).double() + 3.0 * (inb[:, None, None] & inb[None, :, None]
+                                             & inb[None, None, :]).double()
+    del r2
+    gen = torch.Generator(device=dev).manual_seed(5)
+    v5 = torch.clamp(v5 + 0.01 * torch.randn(v5.shape, device=dev, generator=gen,
+                                             dtype=torch.float64) * (v5 > 0), min=0.0).float()
+    return v5
+
+
+def other_configs(sd, dev, timed, world, rank):
+    """C1 / C3 / C4 / C5 of BASELINE.json on this node (parity-test cases in
+    tests/test_gpu_configs.py; reported for context, not the headline).
+    C4 and C5 are sharded over the ranks like the headline; C1 and C3 are
+    single-pose configs and run on rank 0 only (N=1)."""
+    import torch
+    from paper_2208_12737_b200 import DeviceVolume, Detector, pose_frames, render_frames, synthetic
+    from paper_2208_12737_b200.distributed import ShardedDRR, gather_rows, max_over_ranks
+    out = {}
+    # C4: C2 volume, 1024 narrow poses (seed 0), 256^2 @ 2.8125 mm, forward,
+    # images collected on rank 0 through peer stores (and, for comparison, the
+    # NCCL all-gather baseline of the same images)
+    sd4 = sd.with_detector(Detector(256, 256, 2.8125))
+    p4 = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, 1024, seed=0)
+    p4_dev = torch.tensor(p4, device=dev)
+    t = timed(lambda: sd4.render(p4_dev, copy=False), 5, 2)
+    ms = max_over_ranks(float(np.median(t)), dev)
+    out["C4"] = {"workload": f"C2 volume, 1024 narrow poses seed 0, 256x256 @2.8125 mm, forward, "
+                             f"sharded over {world} GPU(s), images (268 MB) stored into rank 0's "
+                             f"buffer by the forward kernels (peer memory)",
+                 "ms_per_batch": ms, "drr_per_s": 1024 / (ms / 1e3)}
+    if world > 1:
+        lo, hi = sd4.shard(1024)
+        fr = pose_frames(p4_dev[lo:hi], sd4.volume.center).detach()
+
+        def nccl_gather():
+            img = render_frames(sd4.volume, sd4.detector, fr)
+            gather_rows(img, 1024)
+        t = timed(nccl_gather, 5, 2)
+        ms = max_over_ranks(float(np.median(t)), dev)
+        out["C4"]["nccl_all_gather_baseline"] = {"ms_per_batch": ms, "drr_per_s": 1024 / (ms / 1e3)}
+    sd4.close()
+    if rank == 0 and world == 1:
+        # C1: 128^3 sphere @ 1 mm, 100^2 @ 2.56 mm, one oblique pose, forward only
+        v1 = DeviceVolume(synthetic.make_phantom("sphere", 128, 1.0), 1.0, device=dev)
+        d1 = Detector(100, 100, 2.56)
+        f1 = pose_frames(torch.tensor([[300.0, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0]], device=dev),
+                         v1.center).detach()
+        t = timed(lambda: render_frames(v1, d1, f1), 20, 3)
+        out["C1"] = {"workload": "128^3 sphere @1 mm, 100x100 @2.56 mm, 1 pose, forward",
+                     "ms_per_drr": float(np.median(t))}
+        # C3: 250-step registration (251 fwd+bwd iterations), one CUDA graph
+        from paper_2208_12737_b200.registration import OptimizerConfig, RegistrationEngine
+        with torch.no_grad():
+            fixed = sd.render(np.asarray([TRUTH]))
+        p0 = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, 1, seed=0)
+        cfg = OptimizerConfig(converged_threshold=-1.1)
+        eng = RegistrationEngine(sd.volume, sd.detector, fixed, 1, cfg)
+
+        def reg_run():
+            eng.reset(p0)
+            eng.run(use_graph=True)
+        reg_run()
+        reg_ms = float(np.median(timed(reg_run, 3, 1)))
+        out["C3"] = {"workload": "slice-to-volume registration on C2: 250 momentum-GD steps "
+                                 "(251 fwd+bwd iterations) of neg-ZNCC, whole loop one CUDA graph",
+                     "ms_total": reg_ms, "ms_per_step": reg_ms / (cfg.max_iters + 1),
+                     "final_neg_zncc": eng.traces()[0].final_loss}
+    # C5: 512^3 @ 0.703125, 1024^2 @ 0.703125, 64 poses fwd+bwd (loss_and_gradient
+    # vs a fixed DRR at the truth pose), sharded, value + grad collected on rank 0
+    v5 = c5_volume(dev) if rank == 0 else None
+    sd5 = ShardedDRR(v5, 0.703125, RHO, 1024, 0.703125, device=dev)
+    del v5
+    fixed5 = sd5.render(np.asarray([TRUTH]))
+    fx = [fixed5.cpu() if rank == 0 else None]
+    if world > 1:
+        import torch.distributed as dist
+        dist.broadcast_object_list(fx, src=0)
+    fixed5 = fx[0][0].to(dev)
+    p5 = torch.tensor(synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, 64, seed=0),
+                      device=dev)
+    t = timed(lambda: sd5.loss_and_gradient(p5, fixed5, copy=False), 3, 1)
+    ms = max_over_ranks(float(np.median(t)), dev)
+    out["C5"] = {"workload": f"512^3 @0.703125 sphere+3x cube+noise, 1024x1024 @0.703125, 64 poses "
+                             f"fwd + neg-ZNCC + bwd, sharded over {world} GPU(s)",
+                 "ms_per_batch": ms, "drr_per_s": 64 / (ms / 1e3)}
+    sd5.close()
+    del sd5
+    torch.cuda.empty_cache()
+    return out
+
+
+# ------------------------------------------------------------------- main
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        return run_reference(args, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2208_12737_b200 import (backward_frames, backward_from_jac, count_steps,
+                                       pose_frames, render_frames, render_frames_jac, synthetic)
+    from paper_2208_12737_b200.distributed import ShardedDRR, max_over_ranks
+
+    # DRR_BENCH_SHARED_GPU=1 (testing only) puts every rank on cuda:0 with the
+    # gloo backend, so the multi-rank path can be exercised on a one-GPU box.
+    shared = os.environ.get("DRR_BENCH_SHARED_GPU") == "1"
+    dev = torch.device("cuda", 0 if shared else local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    # --- volume: built on rank 0, broadcast once (NCCL over NVLink) -------
+    vol_np = synthetic.chest_phantom(DIMS) if rank == 0 else None
+    t0 = time.perf_counter()
+    sd = ShardedDRR(vol_np, SPACING, RHO, H, PITCH, device=dev)
+    torch.cuda.synchronize(dev)
+    bcast_s = time.perf_counter() - t0
+    del vol_np
+
+    GB = args.batch
+    poses = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, GB, seed=0)
+    eta = torch.tensor(poses, device=dev)
+    fixed = sd.render(np.asarray([TRUTH]))
+    fx = [fixed.cpu() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(fx, src=0)
+    fixed = fx[0][0].to(dev)
+    lo, hi = sd.shard(GB)
+    B = hi - lo
+
+    def step():
+        return sd.loss_and_gradient(eta, fixed, "neg_zncc", copy=False)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    timed = make_timer(dev, flush)
 
     # --- warmup + timed steps (device time, per-step events) -------------
     for _ in range(max(args.warmup, 3)):
-        step(eta0)
-        module_step(rot0, tra0)
+        step()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(dev.index) as clk:
-        times = timed(lambda: step(eta0), args.steps, 0)
+        times = timed(step, args.steps, 0)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    local_ms = float(np.mean(times))
-    t = torch.tensor([local_ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_per_step = float(t.item())
-    value = B * world / (ms_per_step / 1e3)
-    module_ms = float(np.mean(timed(lambda: module_step(rot0, tra0), max(10, args.steps // 5), 2)))
+    ms_per_step = max_over_ranks(float(np.mean(times)), dev)
+    value = GB / (ms_per_step / 1e3)
 
-    # --- e2e: public API with pinned host poses in, loss+grads out -------
-    h_eta = torch.tensor(poses_np).pin_memory()
-    h_out = torch.empty((B, 8), dtype=torch.float64).pin_memory()
+    # --- e2e: public API, pinned host poses in, loss + grads back out ------
+    h_eta = torch.tensor(poses).pin_memory()
+    h_val = torch.empty(GB, dtype=torch.float64).pin_memory()
+    h_grad = torch.empty((GB, 7), dtype=torch.float64).pin_memory()
+    d_eta = torch.empty((GB, 7), dtype=torch.float64, device=dev)
 
     def e2e_step():
-        eta = h_eta.to(dev, non_blocking=True)
-        val, grad = step(eta)
-        h_out.copy_(torch.cat([val[:, None], grad], dim=1), non_blocking=True)
+        d_eta[lo:hi].copy_(h_eta[lo:hi], non_blocking=True)  # this rank's poses
+        r = sd.loss_and_gradient(d_eta, fixed, "neg_zncc", copy=False)
+        if r is not None:
+            h_val.copy_(r[0], non_blocking=True)
+            h_grad.copy_(r[1], non_blocking=True)
 
-    e = torch.tensor([float(np.mean(timed(e2e_step, args.steps, 3)))], device=dev,
-                     dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(e, op=dist.ReduceOp.MAX)
-    e2e_value = B * world / (float(e.item()) / 1e3)
-    rot0 = eta0[:, 1:4]
-    tra0 = eta0[:, 4:7]
+    e2e_ms = max_over_ranks(float(np.mean(timed(e2e_step, args.steps, 3))), dev)
+    e2e_value = GB / (e2e_ms / 1e3)
+    if rank == 0:
+        v_ref, g_ref = sd.loss_and_gradient(eta, fixed)
+        torch.cuda.synchronize(dev)
+        assert np.array_equal(h_val.numpy(), v_ref.cpu().numpy()), "e2e values differ"
+        assert np.array_equal(h_grad.numpy(), g_ref.cpu().numpy()), "e2e gradients differ"
+    else:
+        sd.loss_and_gradient(eta, fixed)
 
-    # --- roofline of the dominant kernel (k_forward_jac: the only CT walk) --
-    frames = pose_frames(drr.pose_vectors(rot0, tra0), drr.isocenter).detach()
-    steps_used = count_steps(drr.volume, drr.detector, frames)
-    S = float(steps_used.double().sum().item())  # used voxel-steps in the batch
+    # --- the north-star nn.Module path (torch autograd), rank-local -------
+    from paper_2208_12737_b200 import DRR
+    from paper_2208_12737_b200.metrics import neg_zncc
+    drr = DRR.from_device_volume(sd.volume, RHO, sd.detector, strict=False)
+    rot0, tra0 = eta[lo:hi, 1:4], eta[lo:hi, 4:7]
+    fixed_b = fixed.expand(B, H, W)
+
+    def module_step():
+        rot = rot0.detach().requires_grad_(True)
+        tra = tra0.detach().requires_grad_(True)
+        neg_zncc(drr(rot, tra), fixed_b).sum().backward()
+    module_ms = float(np.mean(timed(module_step, max(10, args.steps // 5), 2)))
+
+    # --- the dominant kernel against the roofline (this rank's shard) ----
+    frames = pose_frames(eta[lo:hi], sd.volume.center).detach()
+    S = float(count_steps(sd.volume, sd.detector, frames).double().sum().item())
     g_img = torch.randn((B, H, W), device=dev, dtype=torch.float32)
-    kt = {"fj": [], "bj": [], "fwd": [], "rewalk": []}
-    jac_holder = {}
+    hold = {}
 
     def k_fj():
-        jac_holder["img"], jac_holder["jac"] = render_frames_jac(drr.volume, drr.detector, frames)
-
+        hold["img"], hold["jac"] = render_frames_jac(sd.volume, sd.detector, frames)
     kfns = {"fj": k_fj,
-            "bj": lambda: backward_from_jac(drr.detector, jac_holder["jac"], g_img),
-            "fwd": lambda: render_frames(drr.volume, drr.detector, frames),
-            "rewalk": lambda: backward_frames(drr.volume, drr.detector, frames, g_img)}
-    for i in range(12):
-        for name in ("fj", "bj", "fwd", "rewalk"):
-            flush.fill_(1.0)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            kfns[name]()
-            e1.record(stream)
-            e1.synchronize()
+            "bj": lambda: backward_from_jac(sd.detector, hold["jac"], g_img),
+            "fwd": lambda: render_frames(sd.volume, sd.detector, frames),
+            "rewalk": lambda: backward_frames(sd.volume, sd.detector, frames, g_img)}
+    kt = {k: [] for k in kfns}
+    for i in range(12):  # interleaved; the first two rounds are warm-up
+        for name, fn in kfns.items():
+            t = timed(fn, 1, 0)
             if i >= 2:
-                kt[name].append(e0.elapsed_time(e1))
+                kt[name].extend(t)
     kms = {k: float(np.mean(v)) for k, v in kt.items()}  # average launch duration, 10 launches
-    fj_ms = kms["fj"]
-    # algorithmic bytes per k_forward_jac launch: one fp32 gather per used
-    # voxel-step + fp32 image store + 6 f64 Jacobian entries per pixel
-    bytes_fj = 4.0 * S + 4.0 * B * H * W + 48.0 * B * H * W
-    bytes_fwd = 4.0 * S + 4.0 * B * H * W  # gathers + image store
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -413,46 +487,45 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None  # dram bytes per k_forward_jac launch from the committed ncu capture
-    limiter = None  # what ncu shows binding that kernel (it is not HBM)
+    # SURVEY 8(d) algorithmic bytes of a forward walk: one fp32 gather per used
+    # voxel-step + the fp32 image store; the stored Jacobian (48 B/pixel, an
+    # artefact of this design) is reported beside it, not counted
+    bytes_8d = 4.0 * S + 4.0 * B * H * W
+    bytes_jac = 48.0 * B * H * W
+    ncu = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)["k_forward_jac"]
-        if tr.get("poses") == B and tr.get("config") == "C2":
-            traffic = float(tr["traffic_bytes_per_launch"])
-            limiter = tr.get("limiter")
+        if tr.get("config") == "C2":
+            per_pose = 1.0 / float(tr["poses"])  # capture scaled to this shard's pose count
+            ncu = {"traffic": float(tr["traffic_bytes_per_launch"]) * per_pose * B,
+                   "lts_bytes": (float(tr["lts_bytes_per_launch"]) * per_pose * B
+                                 if "lts_bytes_per_launch" in tr else None),
+                   "limiter": tr.get("limiter"), "limiter_frac": tr.get("limiter_frac"),
+                   "capture": tr.get("source"), "capture_poses": tr.get("poses")}
     except (OSError, KeyError, ValueError):
         pass
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    achieved_fj = bytes_fj / (fj_ms / 1e3) / 1e9
-
-    # single-pose latency (C2 as configs[1] states it: one pose fwd+bwd)
-    bufs1 = _Buffers(drr.volume, drr.detector, 1)
-    one = timed(lambda: loss_and_gradient(drr.volume, drr.detector, eta0[:1], fixed, "neg_zncc",
-                                          buffers=bufs1), 10, 3)
-    # C3: 250-step registration, whole loop in one CUDA graph
-    from paper_2208_12737_b200.registration import OptimizerConfig, RegistrationEngine
-    reg_cfg = OptimizerConfig(converged_threshold=-1.1)
-    eng = RegistrationEngine(drr.volume, drr.detector, fixed, 1, reg_cfg)
-    eng.reset(poses_np[:1])
-    eng.run(use_graph=True)
-
-    def reg_run():
-        eng.reset(poses_np[:1])
-        eng.run(use_graph=True)
-
-    reg_ms = float(np.median(timed(reg_run, 3, 1)))
-    reg_final = eng.traces()[0].final_loss
+    achieved = bytes_8d / (kms["fj"] / 1e3) / 1e9
+    lts_gbs = (ncu["lts_bytes"] / (kms["fj"] / 1e3) / 1e9) if ncu.get("lts_bytes") else None
 
     if world > 1:
         dist.barrier()
+    other = None
+    if not args.no_other_configs:
+        other = other_configs(sd, dev, timed, world, rank)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(poses, args.cpu_seconds)
+
     if rank != 0:
+        sd.close()
+        dist.barrier()
         dist.destroy_process_group()
         return 0
-
     clocks = clk.summary()
     result = {
-        "metric": "DRRs/sec fwd+bwd (200x200 det, 512x512x133 CT)",
+        "metric": METRIC,
         "value": value,
         "unit": "DRR/s",
         "n_gpus": world,
@@ -460,92 +533,89 @@ def main():
         "warmup": max(args.warmup, 3),
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64 geometry / fp32 CT gathers",
-        "data": "synthetic (chest-shaped CT phantom, SURVEY 8(d))",
-        "config": {"workload": WORKLOAD, "poses_per_gpu": B, "global_batch": B * world,
+        "data": "synthetic (chest-shaped CT phantom, SURVEY 8(d)); random narrow poses",
+        "config": {"workload": WORKLOAD, "global_batch": GB, "poses_per_gpu": B,
                    "detector": [H, W], "ct": list(DIMS), "parallelism": f"pose-shard x{world}",
+                   "collect": "per-pose loss + 7-gradient stored into rank 0's buffers by the "
+                              "kernels (peer memory over NVLink), inside the timed region",
                    "l2": "flushed (256 MiB write) between timed steps, outside the events"},
         "e2e": {"value": e2e_value, "unit": "DRR/s",
-                "h2d_bytes_per_step": int(h_eta.numel() * 8),
-                "d2h_bytes_per_step": int(h_out.numel() * 8)},
+                "h2d_bytes_per_step": int(GB * 7 * 8),
+                "d2h_bytes_per_step": int(GB * 8 * 8),
+                "api": "ShardedDRR.loss_and_gradient: pinned host poses -> device (each rank "
+                       "its shard), loss + gradient read back to pinned host memory on rank 0"},
         "gpu_launches": 6 * args.steps,
-        "module_path": {"api": "DRR nn.Module + metrics.neg_zncc + torch autograd",
+        "module_path": {"api": "DRR nn.Module + metrics.neg_zncc + torch autograd (rank-local)",
                         "ms_per_step": module_ms, "value": B / (module_ms / 1e3)},
-        "roofline": {"bound": "hbm",
+        "roofline": {"bound": "l1",
+                     "roofline_of": "hbm",
                      "kernel": "k_forward_jac (the one CT walk per step: image + ray Jacobian)",
-                     "achieved": achieved_fj, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved_fj / hbm_peak, "traffic": traffic,
-                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same kernel/config)",
-                     "peak_source": peak_src, "limiter": limiter,
-                     "algorithmic_bytes_per_launch": bytes_fj, "launch_ms": fj_ms},
-        "kernels": {"forward_jac_ms": fj_ms, "backward_jac_ms": kms["bj"],
+                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": ncu.get("traffic"),
+                     "lts_gbs": lts_gbs,
+                     "algorithmic_bytes_per_launch": bytes_8d,
+                     "jacobian_store_bytes_per_launch": bytes_jac,
+                     "bytes_rule": "SURVEY 8(d): 4 B per used voxel-step + 4 B per pixel",
+                     "launch_ms": kms["fj"], "poses_per_launch": B,
+                     "peak_source": "measured" if "hbm_gbs" in peaks else "fallback",
+                     "limiter": ncu.get("limiter"), "limiter_frac": ncu.get("limiter_frac"),
+                     "traffic_source": ncu.get("capture")},
+        "kernels": {"forward_jac_ms": kms["fj"], "backward_jac_ms": kms["bj"],
                     "forward_only_ms": kms["fwd"], "rewalk_backward_ms": kms["rewalk"],
                     "voxel_steps_per_drr": S / B,
-                    "voxel_steps_per_s_forward_jac": S / (fj_ms / 1e3),
-                    "voxel_steps_per_s_forward_only": S / (kms["fwd"] / 1e3),
-                    "forward_only_achieved_gbs": bytes_fwd / (kms["fwd"] / 1e3) / 1e9},
-        "single_pose_fwd_bwd_ms": float(np.mean(one)),
-        "registration_c3": {"steps": reg_cfg.max_iters + 1, "ms_total": reg_ms,
-                            "ms_per_step": reg_ms / (reg_cfg.max_iters + 1),
-                            "final_neg_zncc": reg_final, "cuda_graph": True},
+                    "voxel_steps_per_s_forward_jac": S / (kms["fj"] / 1e3),
+                    "voxel_steps_per_s_forward_only": S / (kms["fwd"] / 1e3)},
+        "ct_broadcast_s": bcast_s,
         "clocks": clocks,
     }
-    if world == 1 and not args.no_other_configs:
-        result["other_configs"] = other_configs(dev, drr.volume, timed, flush)
-    if not args.no_cpu_baseline and world == 1:
-        vol_np = vol_np if vol_np is not None else synthetic.chest_phantom(DIMS)
-        kind, worker, fixed_np = cpu_setup(vol_np)
-        procs = os.cpu_count() or 1
-        if args.cpu_sample:
-            n = args.cpu_sample
-        else:  # size the sample to ~15 s of wall time on this host
-            t1, _ = cpu_run(worker, synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS,
-                                                           procs, seed=2), fixed_np, procs)
-            n = procs * max(1, min(64, int(15.0 / max(t1, 1e-3))))
-        poses = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, n, seed=1)
-        wall, res = cpu_run(worker, poses, fixed_np, procs)
-        result["cpu_baseline"] = {
-            "value": n / wall, "unit": "DRR/s", "cores": procs, "kind": kind,
-            "sample": f"{n} poses of C2 loss_and_gradient (neg-ZNCC, native backend, f64), "
-                      f"pose-sharded over {procs} fork processes; {wall:.1f} s wall; "
-                      f"CPU {cpu_model()}"}
+    if other is not None:
+        result["other_configs"] = other
+    if cpu is not None:
+        result["cpu_baseline"] = cpu
     print(json.dumps(result))
+    sd.close()
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
 def run_reference(args, world):
-    """--impl reference: the reference's own CPU path (oracle/_ref, native
-    Cython backend) on this host's cores, same metric/config; rank 0 only."""
+    """--impl reference: the reference's own CPU path (oracle/_ref: drrtrace's
+    loss_and_gradient, native Cython backend) on this host's cores, same
+    metric and poses as the GPU arm; rank 0 only.  The fork pool is created
+    once before the warm-up; each step is one pose per process."""
     from paper_2208_12737_b200 import synthetic
-    vol_np = synthetic.chest_phantom(DIMS)
-    kind, worker, fixed_np = cpu_setup(vol_np)
+    kind, worker = cpu_setup(synthetic.chest_phantom(DIMS))
     procs = os.cpu_count() or 1
-    per_step = procs  # one pose per core per step
-    rng_seed = 0
+    poses = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, args.batch, seed=0)
+    pool = CpuPool(worker, procs)
     times = []
+    k = 0
     for i in range(max(args.warmup, 3) + args.steps):
-        poses = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, per_step,
-                                       seed=rng_seed + i)
-        wall, _ = cpu_run(worker, poses, fixed_np, procs)
+        batch = [poses[(k + j) % len(poses)] for j in range(procs)]
+        k += procs
+        wall, _ = pool.run(batch)
         if i >= max(args.warmup, 3):
             times.append(wall)
+    pool.close()
     ms = 1e3 * float(np.mean(times))
-    value = per_step / (ms / 1e3)
+    value = procs / (ms / 1e3)
     print(json.dumps({
         "impl": "reference",
-        "metric": "DRRs/sec fwd+bwd (200x200 det, 512x512x133 CT)",
+        "metric": METRIC,
         "value": value, "unit": "DRR/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "poses_per_step": per_step,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": args.batch, "poses_per_step": procs,
                    "parallelism": f"{procs} host processes"},
         "cpu_baseline": {"value": value, "unit": "DRR/s", "cores": procs, "kind": kind,
-                         "sample": f"{per_step} poses per step, pose-sharded fork pool; "
-                                   f"CPU {cpu_model()}"},
+                         "sample": f"{procs} poses per step (one per process) cycling through "
+                                   f"the GPU arm's {args.batch}-pose batch, fork pool created "
+                                   f"once before warm-up; CPU {cpu_model()}"},
         "e2e": {"value": value, "unit": "DRR/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }))

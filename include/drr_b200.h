@@ -37,6 +37,13 @@
  *                               (neg_zncc, l2), batched, fused
  *   drr_register_update      <- one iteration of registration.py:89-125
  *                               register() (momentum GD + convergence state)
+ *   drr_peer_export / _open  <- no reference counterpart: the population
+ *   / _close                    study runs independent registrations in
+ *                               parallel processes and collects their traces
+ *                               (cli.py:133-145); here the
+ *                               collecting rank's output buffers are opened by
+ *                               every rank so its kernels store results
+ *                               straight into them over NVLink
  */
 #ifndef DRR_B200_H
 #define DRR_B200_H
@@ -190,6 +197,22 @@ int drr_register_update(double *d_eta, double *d_velocity,
                         int32_t iter, int *d_state, int *d_n_records,
                         double *d_trace_eta, double *d_trace_loss,
                         int32_t n_poses, void *stream);
+
+/* Peer-memory outputs (one node, one process per GPU).  drr_peer_export
+ * describes a device buffer of the calling process (an IPC handle of its
+ * allocation plus the buffer's offset in it); another process passes that
+ * handle to drr_peer_open on its own device and gets a pointer its kernels may
+ * store into (peer access over NVLink is enabled lazily).  drr_peer_close
+ * takes the opened pointer and the handle's offset. */
+typedef struct drr_peer_handle {
+  unsigned char ipc[64];
+  uint64_t offset; /* byte offset of the buffer inside the allocation */
+  uint64_t bytes;  /* bytes from the buffer to the end of the allocation */
+} drr_peer_handle;
+
+int drr_peer_export(const void *d_ptr, drr_peer_handle *out);
+int drr_peer_open(const drr_peer_handle *h, void **d_ptr);
+int drr_peer_close(void *d_ptr, uint64_t offset);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,9 @@ cp -r "$SRC" "$TMP/pkg"
 rm -rf "$OUT"
 python -m pip install --no-index --no-build-isolation --no-deps --quiet \
   --target "$OUT" "$TMP/pkg"
+# the reference's own test files, so tests/test_gpu_reference_suite.py can run
+# them against the "cuda" backend on the GPU box (not committed: _ref/ is ignored)
+cp -r "$SRC/tests" "$OUT/tests"
 python - "$OUT" <<'PY'
 import sys
 sys.path.insert(0, sys.argv[1])

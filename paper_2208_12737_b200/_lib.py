@@ -41,6 +41,9 @@ EXPORTS = (
     "drr_pose_grad",
     "drr_image_loss",
     "drr_register_update",
+    "drr_peer_export",
+    "drr_peer_open",
+    "drr_peer_close",
 )
 
 
@@ -64,6 +67,12 @@ class DrrDetector(ctypes.Structure):
                 ("pitch_x", ctypes.c_double),
                 ("pitch_y", ctypes.c_double),
                 ("ray_split", ctypes.c_int32)]
+
+
+class DrrPeerHandle(ctypes.Structure):
+    _fields_ = [("ipc", ctypes.c_ubyte * 64),
+                ("offset", ctypes.c_uint64),
+                ("bytes", ctypes.c_uint64)]
 
 
 _vp = ctypes.c_void_p
@@ -90,6 +99,9 @@ _SIGNATURES = {
     "drr_image_loss": ([_vp, _vp, _int, _i64, _i32, _i64, _int, _vp, _vp, _vp, _vp], _int),
     "drr_register_update": ([_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(DrrRegConfig), _i32,
                              _vp, _vp, _vp, _vp, _i32, _vp], _int),
+    "drr_peer_export": ([_vp, ctypes.POINTER(DrrPeerHandle)], _int),
+    "drr_peer_open": ([ctypes.POINTER(DrrPeerHandle), ctypes.POINTER(_vp)], _int),
+    "drr_peer_close": ([_vp, ctypes.c_uint64], _int),
 }
 
 DRR_LOSS_NEG_ZNCC = 0

@@ -21,9 +21,18 @@ The volume stays float64 on this path (``DRR_VOL_F64``) so energies are
 bit-identical to the reference's native backend.  Inputs are coerced with
 ``np.ascontiguousarray(..., float64)`` like the reference (``_native.pyx:142-145``);
 outputs are fresh numpy arrays owned by the caller.
+
+The reference's dispatchers call a backend once per chunk of rays
+(``raytrace.py:96-103,122-128``: 16384 rays, 2048 for the gradient) with the
+same ``volume.flat_data()`` each time, so the device copy of a READ-ONLY flat
+volume (the reference's ``Volume`` freezes its data, ``volume.py:52``) is
+cached, keyed on its buffer and geometry; a writeable array is uploaded on
+every call (its contents may change between calls).
 """
 
 from __future__ import annotations
+
+import warnings
 
 import numpy as np
 import torch
@@ -41,14 +50,39 @@ def _device():
 
 
 def _upload(arr, dev):
-    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(dev)
+    arr = np.ascontiguousarray(arr, dtype=np.float64)
+    with warnings.catch_warnings():  # read-only host arrays are only read (copied to the device)
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(arr).to(dev)
+
+
+# (buffer address, bytes, dtype, dims, device) -> (the host array, kept alive so
+# the address cannot be reused while cached; its device copy); last few volumes
+_VOL_CACHE: dict = {}
+_VOL_CACHE_MAX = 2
+
+
+def _device_volume(flat_data, dims, dev):
+    arr = np.asarray(flat_data).reshape(-1)
+    if arr.flags.writeable:
+        return _upload(arr, dev)
+    key = (arr.__array_interface__["data"][0], arr.nbytes, arr.dtype.str,
+           tuple(int(n) for n in dims), str(dev))
+    hit = _VOL_CACHE.get(key)
+    if hit is not None:
+        return hit[1]
+    while len(_VOL_CACHE) >= _VOL_CACHE_MAX:
+        _VOL_CACHE.pop(next(iter(_VOL_CACHE)))
+    d = _upload(arr, dev)
+    _VOL_CACHE[key] = (arr, d)
+    return d
 
 
 def _prep(flat_data, dims, spacing, origin, source, pixels):
     dev = _device()
     pix = np.ascontiguousarray(np.atleast_2d(pixels), dtype=np.float64)
     grid = _lib.make_grid(dims, spacing, origin)
-    vol = _upload(np.asarray(flat_data).reshape(-1), dev)
+    vol = _device_volume(flat_data, dims, dev)
     src = _upload(np.asarray(source).reshape(3), dev)
     return dev, grid, vol, src, _upload(pix, dev), pix.shape[0]
 

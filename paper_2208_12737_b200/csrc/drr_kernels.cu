@@ -672,22 +672,41 @@ int make_det(const drr_detector* in, drr::DetDev& d) {
   return DRR_OK;
 }
 
+// Streaming multiprocessors of the current device (cudaDevAttrMultiProcessorCount,
+// cached per device): the auto ray split and the pose-group size below are
+// sized in waves of resident CTAs, so a MIG slice or another SKU gets its own.
+int device_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1)
+      n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+constexpr int kResidentCtasPerSm = 6;  // the walk kernels' launch bounds (DRR_*_MINB)
+
 // Threads per ray: explicit, or auto = the smallest K in {1, 2, 4, 8} with
-// B*H*W*K >= one wave of resident threads (148 SMs x 6 CTAs x 128).  A/B
-// (scripts/kbench_split.py, one pose, fwd+jac+contraction / forward ms for
-// K = 1 / 2 / 4 / 8): C2 200^2 0.218 / 0.150 / 0.147 / 0.161 and 0.171 /
-// 0.114 / 0.112 / 0.124 (K = 4 chosen; two waves would pick 8); C1 100^2
-// forward 0.057 / 0.047 / 0.039 / 0.034 (K = 8).
+// B*H*W*K >= one wave of resident threads (SMs x 6 CTAs x 128; 148 SMs on a
+// B200).  A/B (scripts/kbench_split.py, one pose, fwd+jac+contraction /
+// forward ms for K = 1 / 2 / 4 / 8): C2 200^2 0.218 / 0.150 / 0.147 / 0.161
+// and 0.171 / 0.114 / 0.112 / 0.124 (K = 4 chosen; two waves would pick 8);
+// C1 100^2 forward 0.057 / 0.047 / 0.039 / 0.034 (K = 8).
 int ray_split(const drr::DetDev& d, int n_poses) {
   if (d.split > 0) return d.split;
   const double rays = static_cast<double>(n_poses) * d.H * d.W;
+  const double wave = static_cast<double>(device_sms()) * kResidentCtasPerSm * drr::kThreads;
   int k = 1;
-  while (k < 8 && rays * k < 148.0 * 6.0 * 128.0) k *= 2;
+  while (k < 8 && rays * k < wave) k *= 2;
   return k;
 }
 
 // Poses interleaved tile by tile in the CTA order (DetDev::pose_group):
-// groups of ~16K CTAs (G = 16384 / tiles per pose).  Interleaving pays when a
+// groups of ~18 waves of resident CTAs (16384 CTAs on a 148-SM B200, scaled by
+// the SM count: G = 16384 x SMs / 148 / tiles per pose).  Interleaving pays when a
 // tile's CT footprint is large next to the pose spread (nearby poses share
 // it), and costs when tiles are many and small (each pose then brings its own
 // lines).  A/B (scripts/gpu_ab_fast.sh, gpu_ab_configs.sh; fwd+jac ms or
@@ -700,7 +719,8 @@ int ray_split(const drr::DetDev& d, int n_poses) {
 #define DRR_POSE_GROUP 0
 #endif
 int pose_group(int n_poses, unsigned tiles) {
-  long G = DRR_POSE_GROUP > 0 ? DRR_POSE_GROUP : 16384L / (tiles > 0 ? tiles : 1);
+  const long group_ctas = 16384L * device_sms() / 148;
+  long G = DRR_POSE_GROUP > 0 ? DRR_POSE_GROUP : group_ctas / (tiles > 0 ? tiles : 1);
   return static_cast<int>(G < 1 ? 1 : (G > n_poses ? n_poses : G));
 }
 
@@ -1092,6 +1112,8 @@ int drr_register_update(double* d_eta, double* d_velocity, const double* d_grad_
       d_trace_eta, d_trace_loss, n_poses);
   return check_launch("drr_register_update");
 }
+
+#include "peer_memory.cuh"
 
 }  // extern "C"
 #endif  // DRR_KERNELS_ONLY

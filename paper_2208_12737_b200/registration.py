@@ -105,14 +105,20 @@ class _Buffers:
         self.ws = torch.empty(max(self.ws_bytes, 8), dtype=torch.uint8, device=dev)
 
 
-def _launch_loss_grad(lib, vol, det, iso, eta, fixed, fixed_stride, kind, buf, stream):
+def _launch_loss_grad(lib, vol, det, iso, eta, fixed, fixed_stride, kind, buf, stream,
+                      value_ptr=None):
+    """pose frames -> forward + ray Jacobian -> loss value and pixel gradient ->
+    contraction to dL/dframe (buf.grad_frames).  The loss values go to
+    ``value_ptr`` when given (e.g. another rank's buffer, distributed.PeerRows),
+    else to buf.value."""
     B = buf.B
+    value_ptr = buf.value.data_ptr() if value_ptr is None else value_ptr
     _lib.check(lib.drr_pose_frames(eta.data_ptr(), B, iso, buf.frames.data_ptr(), stream))
     _lib.check(lib.drr_forward_jac(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
                                    buf.frames.data_ptr(), B, det.c, buf.img.data_ptr(), 0,
                                    buf.jac.data_ptr(), stream))
     _lib.check(lib.drr_image_loss(buf.img.data_ptr(), fixed.data_ptr(), 0, fixed_stride, B,
-                                  det.height * det.width, kind, buf.value.data_ptr(),
+                                  det.height * det.width, kind, value_ptr,
                                   buf.pix_grad.data_ptr(), buf.status.data_ptr(), stream))
     _lib.check(lib.drr_backward_jac(buf.jac.data_ptr(), B, det.c, buf.pix_grad.data_ptr(), 0,
                                     buf.grad_frames.data_ptr(), buf.ws.data_ptr(),

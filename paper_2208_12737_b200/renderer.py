@@ -75,6 +75,21 @@ class DeviceVolume:
         arr = np.asarray(flat).reshape(tuple(int(n) for n in dims)[::-1])  # (nz, ny, nx)
         return cls(np.transpose(arr, (2, 1, 0)), spacing, origin, device, dtype)
 
+    @classmethod
+    def empty(cls, dims, spacing, origin=(0.0, 0.0, 0.0), device=None, dtype=torch.float32):
+        """Uninitialised device volume of the given dims (filled by the caller,
+        e.g. a broadcast of another rank's ``flat``)."""
+        self = cls.__new__(cls)
+        self.dims = tuple(int(n) for n in dims)
+        self.spacing = tuple(float(s) for s in np.broadcast_to(np.asarray(spacing, np.float64), (3,)))
+        self.origin = tuple(float(s) for s in np.broadcast_to(np.asarray(origin, np.float64), (3,)))
+        self.dtype = dtype
+        device = torch.device(device) if device is not None else torch.device("cuda")
+        self.flat = torch.empty(int(np.prod(self.dims)), dtype=dtype, device=device)
+        self.vol_dtype = _lib.DRR_VOL_F32 if dtype == torch.float32 else _lib.DRR_VOL_F64
+        self.grid = _lib.make_grid(self.dims, self.spacing, self.origin)
+        return self
+
     @property
     def center(self):
         return volume_center(self.dims, self.spacing, self.origin)
@@ -313,6 +328,21 @@ class DRR(torch.nn.Module):
         self.isocenter = tuple(self.volume.center if isocenter is None else
                                (float(v) for v in isocenter))
         self.strict = strict
+
+    @classmethod
+    def from_device_volume(cls, volume: DeviceVolume, sdr: float, detector: Detector,
+                           isocenter=None, strict: bool = True) -> "DRR":
+        """A module over an already resident volume (e.g. one broadcast by
+        distributed.ShardedDRR): no upload, no copy."""
+        self = cls.__new__(cls)
+        torch.nn.Module.__init__(self)
+        if not (float(sdr) > 0 and np.isfinite(float(sdr))):
+            raise InvalidArgumentError(f"sdr must be positive, got {sdr}")
+        self.volume, self.detector, self.sdr = volume, detector, float(sdr)
+        self.isocenter = tuple(volume.center if isocenter is None else
+                               (float(v) for v in isocenter))
+        self.strict = strict
+        return self
 
     @property
     def height(self):
