@@ -328,6 +328,25 @@ def other_configs(sd, dev, timed, world, rank):
             eng.run(use_graph=True)
         reg_run()
         reg_ms = float(np.median(timed(reg_run, 3, 1)))
+        # central finite differences reported alongside (north star):
+        # default_fd_steps, float64 renders, boundary attribution (fd.fd_report)
+        from paper_2208_12737_b200.fd import fd_report
+        fd = {}
+        eta2 = np.array([RHO, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0])  # C2's single pose
+        r2 = fd_report(sd.volume, sd.detector, eta2, fixed.double().cpu().numpy())
+        fixed1 = render_frames(v1, d1, pose_frames(torch.tensor([[300.0, 0.45, 1.25, 0.1, 0.0, 0.0,
+                                                                   0.0]], device=dev),
+                                                   v1.center).detach(),
+                               out_dtype=torch.float64)[0].cpu().numpy()
+        r1 = fd_report(v1, d1, np.array([300.0, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0]), fixed1)
+        for name, r in (("C2", r2), ("C1", r1)):
+            fd[name] = {k: r[k] for k in ("max_rel_kink_free", "n_kink_free", "boundary",
+                                          "unexplained", "rel")}
+        out["fd_check"] = {"method": "central FD, default_fd_steps (gradients.py:72-74), "
+                                     "float64 renders; components whose stencil crosses a "
+                                     "traversal-structure change (detect_fd_boundaries) are "
+                                     "excluded; the reference's bar is rel < 1e-5",
+                           **fd}
         out["C3"] = {"workload": "slice-to-volume registration on C2: 250 momentum-GD steps "
                                  "(251 fwd+bwd iterations) of neg-ZNCC, whole loop one CUDA graph",
                      "ms_total": reg_ms, "ms_per_step": reg_ms / (cfg.max_iters + 1),
@@ -424,6 +443,12 @@ def main():
         dist.barrier()
     ms_per_step = max_over_ranks(float(np.mean(times)), dev)
     value = GB / (ms_per_step / 1e3)
+    # native launches per step on each rank (registration._Buffers picks the chain)
+    mode = next(b.mode for k, b in sd._bufs.items() if k[0] == "lg")
+    launches_per_step = 6 if mode == "jac" else 4
+    chain = ("jac: pose_frames, forward_jac, image_loss, backward_jac, reduce_frames, pose_grad"
+             if mode == "jac" else
+             "fused: pose_frames, forward_loss, image_loss, reduce_loss_grad")
 
     # --- e2e: public API, pinned host poses in, loss + grads back out ------
     h_eta = torch.tensor(poses).pin_memory()
@@ -547,7 +572,8 @@ def main():
                 "d2h_bytes_per_step": int(GB * 8 * 8),
                 "api": "ShardedDRR.loss_and_gradient: pinned host poses -> device (each rank "
                        "its shard), loss + gradient read back to pinned host memory on rank 0"},
-        "gpu_launches": 6 * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
+        "step_chain": chain,
         "module_path": {"api": "DRR nn.Module + metrics.neg_zncc + torch autograd (rank-local)",
                         "ms_per_step": module_ms, "value": B / (module_ms / 1e3)},
         "roofline": {"bound": "l1",

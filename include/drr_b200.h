@@ -28,6 +28,8 @@
  *                               contraction, down to the 12-number frame
  *   drr_count_steps          <- _kernels/python_ref.py:191-201 ray_structure
  *                               (number of used voxel-steps per ray)
+ *   drr_signature            <- gradients.py:124-142 discrete_signature (the
+ *                               traversal structure of every ray, hashed)
  *   drr_pose_frames          <- geometry.py:120-149 _pose_frame (+ the
  *                               isocenter offset of geometry.py:166-175), batched
  *   drr_pose_grad            <- the tangent half of the same map (dual.py
@@ -35,6 +37,9 @@
  *                               -> dL/d(rho, theta, phi, gamma, bx, by, bz)
  *   drr_image_loss           <- metrics.py:71-91 loss_value_and_pixel_grad
  *                               (neg_zncc, l2), batched, fused
+ *   drr_forward_loss_grad    <- gradients.py:61-69 loss_and_gradient for the
+ *                               two losses of metrics.py:71-91, batched: one
+ *                               walk per ray, no stored Jacobian
  *   drr_register_update      <- one iteration of registration.py:89-125
  *                               register() (momentum GD + convergence state)
  *   drr_peer_export / _open  <- no reference counterpart: the population
@@ -152,6 +157,15 @@ int drr_count_steps(const void *d_vol, int vol_dtype, const drr_grid *grid,
                     const double *d_frames, int32_t n_poses,
                     const drr_detector *det, int32_t *d_steps, void *stream);
 
+/* Per-pose 64-bit signature of the discrete traversal structure of all its
+ * rays (crossing labels in merge order, used segments, their voxels, the
+ * exit selector; python_ref.py:191-201 ray_structure).  Equal signatures =
+ * the same smooth branch of the energy map (detect_fd_boundaries,
+ * gradients.py:145-167).  d_sig: B uint64. */
+int drr_signature(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                  const double *d_frames, int32_t n_poses,
+                  const drr_detector *det, uint64_t *d_sig, void *stream);
+
 /* B x 7 pose vectors (rho, theta, phi, gamma, bx, by, bz) -> B x 12 frames.
  * isocenter: 3 doubles in HOST memory (the volume centre). */
 int drr_pose_frames(const double *d_eta, int32_t n_poses,
@@ -172,6 +186,26 @@ int drr_image_loss(const void *d_img, const void *d_fixed, int img_dtype,
                    int64_t fixed_stride, int32_t n_images, int64_t npix,
                    int kind, double *d_value, float *d_grad, int *d_status,
                    void *stream);
+
+/* A whole neg-ZNCC / L2 loss-and-gradient step for B poses with ONE walk per
+ * ray and no stored ray Jacobian: the walk writes the image (img_dtype 0 =
+ * float32, 1 = float64; d_fixed has the same dtype, fixed_stride 0 = one
+ * fixed image for all, H*W = one per pose) and per-CTA sums of the ray
+ * Jacobian weighted by 1, the image value and the fixed value; the loss
+ * kernel gives value / status (as drr_image_loss) and the pixel gradient as an
+ * affine map of the two images; a fixed-order reduction combines them into
+ * d_grad_frames (B x 12) and, given d_eta, d_grad_eta (B x 7).  Either
+ * gradient output may be NULL.  Undefined metrics (status 1) give NaN.
+ * Workspace: drr_loss_grad_workspace_size. */
+size_t drr_loss_grad_workspace_size(int32_t n_poses, const drr_detector *det);
+int drr_forward_loss_grad(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                          const double *d_frames, const double *d_eta,
+                          int32_t n_poses, const drr_detector *det,
+                          const void *d_fixed, int64_t fixed_stride, int kind,
+                          void *d_img, int img_dtype, double *d_value,
+                          int *d_status, double *d_grad_frames,
+                          double *d_grad_eta, void *d_workspace,
+                          size_t workspace_bytes, void *stream);
 
 /* Momentum gradient descent settings (registration.py:41-58). */
 typedef struct drr_reg_config {

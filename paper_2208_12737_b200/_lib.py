@@ -37,10 +37,13 @@ EXPORTS = (
     "drr_forward_jac",
     "drr_backward_jac",
     "drr_count_steps",
+    "drr_signature",
     "drr_pose_frames",
     "drr_pose_grad",
     "drr_image_loss",
     "drr_register_update",
+    "drr_loss_grad_workspace_size",
+    "drr_forward_loss_grad",
     "drr_peer_export",
     "drr_peer_open",
     "drr_peer_close",
@@ -94,11 +97,15 @@ _SIGNATURES = {
     "drr_forward_jac": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp, _vp], _int),
     "drr_backward_jac": ([_vp, _i32, _DP, _vp, _int, _vp, _vp, _sz, _vp], _int),
     "drr_count_steps": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
+    "drr_signature": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
     "drr_pose_frames": ([_vp, _i32, ctypes.POINTER(ctypes.c_double), _vp, _vp], _int),
     "drr_pose_grad": ([_vp, _vp, _i32, _vp, _vp], _int),
     "drr_image_loss": ([_vp, _vp, _int, _i64, _i32, _i64, _int, _vp, _vp, _vp, _vp], _int),
     "drr_register_update": ([_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(DrrRegConfig), _i32,
                              _vp, _vp, _vp, _vp, _i32, _vp], _int),
+    "drr_loss_grad_workspace_size": ([_i32, _DP], _sz),
+    "drr_forward_loss_grad": ([_vp, _int, _GP, _vp, _vp, _i32, _DP, _vp, _i64, _int, _vp, _int,
+                               _vp, _vp, _vp, _vp, _vp, _sz, _vp], _int),
     "drr_peer_export": ([_vp, ctypes.POINTER(DrrPeerHandle)], _int),
     "drr_peer_open": ([ctypes.POINTER(DrrPeerHandle), ctypes.POINTER(_vp)], _int),
     "drr_peer_close": ([_vp, ctypes.c_uint64], _int),

@@ -36,8 +36,7 @@ from .errors import (GradientUndefinedError, InvalidArgumentError, KernelError,
                      MetricUndefinedError)
 from .geometry import MIN_ABS_SIN_PHI
 from .registration import OptimizerConfig, RegistrationTrace, RegistrationEngine
-from .renderer import (Detector, DeviceVolume, backward_from_jac, render_frames,
-                       render_frames_jac, _stream_ptr)
+from .renderer import Detector, DeviceVolume, render_frames, render_frames_jac, _stream_ptr
 
 __all__ = ["Volume", "PoseParameters", "DetectorSpec", "Image", "GradientRecord",
            "OptimizerConfig", "RegistrationTrace", "render", "render_iterative",
@@ -237,30 +236,6 @@ def _check_pose(pose) -> None:
             f"pose is gimbal-degenerate: |sin(phi)| <= {MIN_ABS_SIN_PHI} at phi={pose.phi}")
 
 
-def _loss_value_and_pixel_grad(kind: str, moving: torch.Tensor, fixed: torch.Tensor):
-    """metrics.py:71-91 in float64 on the device (population sigma, the
-    reference's analytic pixel gradient; zero variance raises)."""
-    if moving.shape != fixed.shape:
-        raise InvalidArgumentError(f"image shapes differ: {tuple(moving.shape)} vs {tuple(fixed.shape)}")
-    if kind == "neg_zncc":
-        def std(x, which):
-            mu = x.mean()
-            sigma = torch.sqrt(((x - mu) ** 2).mean())
-            if float(sigma) == 0.0:
-                raise MetricUndefinedError(f"{which} image has zero variance")
-            return (x - mu) / sigma, sigma
-        a_hat, sa = std(moving, "moving")
-        b_hat, _ = std(fixed, "fixed")
-        raw = (a_hat * b_hat).mean()
-        value = -float(min(1.0, max(-1.0, float(raw))))
-        return value, -(b_hat - raw * a_hat) / (moving.numel() * sa)
-    if kind == "l2":
-        diff = moving - fixed
-        value = float(torch.linalg.norm(diff.reshape(-1)))
-        return value, (torch.zeros_like(diff) if value == 0.0 else diff / value)
-    raise InvalidArgumentError(f"loss kind must be one of ('neg_zncc', 'l2'), got {kind!r}")
-
-
 def _check_backend(backend) -> None:
     if backend not in (None, "cuda"):
         raise InvalidArgumentError(f"this module renders on the GPU only; backend={backend!r}")
@@ -312,29 +287,58 @@ def render_with_gradient(volume, pose, spec, backend=None):
 def loss_and_gradient(volume, pose, spec, fixed_image, loss_kind: str = "neg_zncc",
                       backend=None) -> GradientRecord:
     """gradients.py:61-69: loss of the DRR against ``fixed_image`` and its
-    exact 7-gradient, reduced over pixels in a fixed order."""
+    exact 7-gradient, reduced over pixels in a fixed order.  One native call
+    (``drr_forward_loss_grad``, float64 image and fixed image): one walk per
+    ray, the loss on the device, no stored Jacobian; one host read at the end."""
+    from .registration import LOSS_KINDS
     _check_backend(backend)
     _check_pose(pose)
-    dv, det, eta, img, jac = _render_jac(volume, pose, spec)
-    fixed = torch.as_tensor(np.asarray(getattr(fixed_image, "values", fixed_image),
-                                       dtype=np.float64), device=dv.device)
-    value, pix_grad = _loss_value_and_pixel_grad(loss_kind, img, fixed)
-    grad_frames = backward_from_jac(det, jac, pix_grad[None])   # (1, 12)
-    ge = torch.empty((1, 7), dtype=torch.float64, device=dv.device)
-    e = torch.tensor(eta[None], dtype=torch.float64, device=dv.device)
-    _lib.check(_lib.load().drr_pose_grad(e.data_ptr(), grad_frames.data_ptr(), 1, ge.data_ptr(),
-                                         _stream_ptr(dv.device)))
-    return GradientRecord(value=value, grad=ge[0].cpu().numpy())
-
-
-def register(fixed_image, volume, pose0, spec, config: OptimizerConfig | None = None):
-    """registration.py:89-125: momentum GD from ``pose0``; the loop runs on the
-    device (RegistrationEngine, one CUDA graph)."""
-    config = config or OptimizerConfig()
-    dv = _device_volume(volume)
+    if loss_kind not in LOSS_KINDS:
+        raise InvalidArgumentError(f"loss kind must be one of ('neg_zncc', 'l2'), got {loss_kind!r}")
     fixed = np.asarray(getattr(fixed_image, "values", fixed_image), dtype=np.float64)
+    if fixed.shape != (spec.height, spec.width):
+        raise InvalidArgumentError(
+            f"image shapes differ: {(spec.height, spec.width)} vs {fixed.shape}")
+    dv = _device_volume(volume)
+    eta = _eta(pose)
+    dev = dv.device
+    f = _frames(eta, tuple(spec.isocenter), dev)
+    det = _detector(spec)
+    lib = _lib.load()
+    e = torch.tensor(eta[None], dtype=torch.float64, device=dev)
+    fx = torch.as_tensor(fixed, device=dev)
+    img = torch.empty((1, spec.height, spec.width), dtype=torch.float64, device=dev)
+    out = torch.empty(9, dtype=torch.float64, device=dev)   # value, status, grad (7)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws_bytes = lib.drr_loss_grad_workspace_size(1, det.c)
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=dev)
+    _lib.check(lib.drr_forward_loss_grad(
+        dv.flat.data_ptr(), dv.vol_dtype, dv.grid, f.data_ptr(), e.data_ptr(), 1, det.c,
+        fx.data_ptr(), 0, LOSS_KINDS[loss_kind], img.data_ptr(), 1, out.data_ptr(),
+        status.data_ptr(), None, out[2:].data_ptr(), ws.data_ptr(), ws_bytes, _stream_ptr(dev)))
+    out[1] = status[0].to(torch.float64)
+    host = out.cpu().numpy()
+    if host[1] != 0:
+        raise MetricUndefinedError("moving or fixed image has zero variance")
+    return GradientRecord(value=float(host[0]), grad=host[2:].copy())
+
+
+def register(fixed_image, volume, pose0, spec, config=None):
+    """registration.py:89-125: momentum GD from ``pose0``; the loop runs on the
+    device (RegistrationEngine, one CUDA graph), rendering and scoring in
+    float64 as the reference does.  ``config`` may be this module's or the
+    reference's OptimizerConfig.  Like the reference, a pose where the loss is
+    undefined -- here also a fixed image of the wrong shape -- ends the run
+    as failed instead of raising."""
+    config = config or OptimizerConfig()
+    eta0 = _eta(pose0)
+    fixed = np.asarray(getattr(fixed_image, "values", fixed_image), dtype=np.float64)
+    if fixed.shape != (spec.height, spec.width):   # metrics._check_pair raises -> failed run
+        return RegistrationTrace(rho=float(eta0[0]), poses=eta0[None, 1:].copy(),
+                                 losses=np.array([np.inf]), converged=False, failed=True)
+    dv = _device_volume(volume)
     eng = RegistrationEngine(dv, _detector(spec), fixed, 1, config,
-                             isocenter=tuple(spec.isocenter))
-    eng.reset(_eta(pose0)[None])
+                             isocenter=tuple(spec.isocenter), image_dtype=torch.float64)
+    eng.reset(eta0[None])
     eng.run(use_graph=True)
     return eng.traces()[0]

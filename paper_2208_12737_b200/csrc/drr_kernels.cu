@@ -422,6 +422,210 @@ __global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
   }
 }
 
+// ------------------------------------------ forward + fused loss gradient
+// One walk per ray for a whole neg-ZNCC / L2 loss-and-gradient step
+// (gradients.py:61-69 with metrics.py:71-91), with no per-ray Jacobian stored.
+// Both losses have a pixel gradient that is affine in the two images,
+// dL/da_i = c0 + c1 a_i + c2 b_i (k_image_loss's coefficients), so
+//   dL/dframe = c0 sum_i J_i + c1 sum_i a_i J_i + c2 sum_i b_i J_i
+// with J_i the ray's 12-vector (dE/ds, dE/dp, a_h dE/dp, a_w dE/dp).  The
+// walk knows a_i (its own image value, as stored), b_i (the fixed image) and
+// J_i, so each CTA reduces the three 12-vectors over its pixels in a fixed
+// order and writes 36 doubles; k_reduce_loss_grad combines the CTAs
+// (fixed order) with the coefficients once the loss kernel has run.  That
+// removes the 48 B/pixel Jacobian store and its re-read (k_backward_jac) from
+// the step, and any batch size takes the one-walk path.
+constexpr int kLossSums = 3 * kFrameGrads;
+template <typename VT, typename OT, int K>
+__global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
+    k_forward_loss(const VT* __restrict__ vol, const GridDev g,
+                   const double* __restrict__ frames, const DetDev det,
+                   OT* __restrict__ img, const OT* __restrict__ fixed, int64_t fixed_stride,
+                   double* __restrict__ partials) {
+  extern __shared__ __align__(16) double tab[];
+  __shared__ int arrivals;  // warps done with the walk (the last one reduces)
+  if (threadIdx.x == 0) arrivals = 0;
+  build_plane_table(g, frames + 12 * cta_pos(det).b, tab);  // s of this CTA's pose
+  __syncthreads();
+  int h, w, chunk;
+  tile_ray<K>(det, h, w, chunk);
+  const bool valid = h < det.H && w < det.W;
+  const int b = cta_pos(det).b;
+  double part[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  if (valid) {
+    double s[3], p[3], ah, aw;
+    pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
+    Ray r;
+    ray_setup(g, s, p, r, K, chunk);
+    if (r.hit) {
+      LeanSums o;
+      walk_sums<VT, kLeanGrad, (K > 1)>(vol, g, tab, r, o);
+      part[0] = o.acc;
+      part[1] = o.G0; part[2] = o.G1; part[3] = o.G2;
+      part[4] = o.H0; part[5] = o.H1; part[6] = o.H2;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 7; ++k) part[k] = chunk_sum<K>(part[k]);
+  // the pixel again (volatile index reads): nothing of it is held across the walk
+  tile_ray<K>(det, h, w, chunk);
+  const int bp = cta_pos(det).b;
+  double J[kFrameGrads], av = 0.0, bv = 0.0;
+#pragma unroll
+  for (int k = 0; k < kFrameGrads; ++k) J[k] = 0.0;
+  if (h < det.H && w < det.W && chunk == 0) {
+    const size_t pix = (static_cast<size_t>(bp) * det.H + h) * det.W + w;
+    double d[3], ah, aw;
+    reload_ray_d(frames + 12 * bp, det, h, w, d, ah, aw);
+    const double L = ray_length(d);
+    const OT e = static_cast<OT>(L * part[0]);
+    img[pix] = e;
+    av = static_cast<double>(e);  // the value the loss kernel reads
+    bv = static_cast<double>(fixed[static_cast<size_t>(bp) * fixed_stride +
+                                   static_cast<size_t>(h) * det.W + w]);
+    if (part[0] != 0.0 || part[1] != 0.0 || part[2] != 0.0 || part[3] != 0.0 ||
+        part[4] != 0.0 || part[5] != 0.0 || part[6] != 0.0) {
+      double dEds[3], dEdp[3];
+      sums_to_endpoint_grads(d, part[0], part + 1, part + 4, L, dEds, dEdp);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        J[a] = dEds[a];
+        J[3 + a] = dEdp[a];
+        J[6 + a] = ah * dEdp[a];
+        J[9 + a] = aw * dEdp[a];
+      }
+    }
+  }
+  // Fixed-order CTA sums of w * J for w = 1, a, b: xor butterfly in each warp
+  // (all 36 chains independent), then the 4 warps in index order -- summed by
+  // whichever warp finishes last (a shared-memory arrival count), so no warp
+  // waits at a CTA barrier for the slowest walk of its CTA (A/B: a barrier
+  // here made the kernel ~4% slower than k_forward_jac, whose warps exit as
+  // soon as their walks end).
+  __shared__ double warp_part[kThreads / 32][kLossSums];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int wsel = 0; wsel < 3; ++wsel) {
+    const double wt = wsel == 0 ? 1.0 : (wsel == 1 ? av : bv);
+    double v[kFrameGrads];
+#pragma unroll
+    for (int k = 0; k < kFrameGrads; ++k) v[k] = wsel == 0 ? J[k] : wt * J[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < kFrameGrads; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < kFrameGrads; ++k) warp_part[warp][wsel * kFrameGrads + k] = v[k];
+  }
+  int last = 0;
+  if (lane == 0) {
+    __threadfence_block();  // this warp's row before its arrival
+    last = atomicAdd(&arrivals, 1) == kThreads / 32 - 1;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence_block();  // every other warp's row after their arrivals
+  const int blocks_per_pose = gridDim.x * gridDim.y;
+  const CtaPos c = cta_pos(det);
+  const int blk = c.ty * gridDim.x + c.tx;
+  double* out = partials + (static_cast<size_t>(c.b) * blocks_per_pose + blk) * kLossSums;
+  for (int t = lane; t < kLossSums; t += 32) {
+    const volatile double* col = &warp_part[0][t];
+    double sacc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kThreads / 32; ++q) sacc += col[q * kLossSums];
+    out[t] = sacc;
+  }
+}
+
+// ------------------------------------------------------ discrete signature
+// Per pose, a 64-bit signature of every ray's traversal structure (SigVisitor:
+// labels, used set, voxels, exit selector; a missed ray hashes as a miss),
+// combined over the pixels by addition mod 2^64 of mix(pixel, ray hash) --
+// order-free, so the atomics give the same bits every run.  Replaces
+// gradients.py:124-142 discrete_signature for detect_fd_boundaries
+// (gradients.py:145-167).  One thread per ray, the v4 visitor walk.
+template <typename VT>
+__global__ void __launch_bounds__(kThreads)
+    k_signature(const VT* __restrict__ vol, const GridDev g, const double* __restrict__ frames,
+                const DetDev det, unsigned long long* __restrict__ sig) {
+  extern __shared__ __align__(16) double tab[];
+  build_plane_table(g, frames + 12 * cta_pos(det).b, tab);
+  __syncthreads();
+  int h, w, chunk;
+  tile_ray<1>(det, h, w, chunk);
+  const int b = cta_pos(det).b;
+  uint64_t v = 0;
+  if (h < det.H && w < det.W) {
+    double s[3], p[3], ah, aw;
+    pixel_ray(frames + 12 * b, det, h, w, s, p, ah, aw);
+    Ray r;
+    ray_setup(g, s, p, r);
+    SigVisitor vis;
+    if (r.hit) {
+      vis.h = sig_mix(vis.h, static_cast<uint64_t>(r.lab_min));
+      walk_select<VT, false>(vol, g, tab, r, vis);
+    } else {
+      vis.h = sig_mix(vis.h, 0xDEADull);  // miss
+    }
+    v = sig_mix(static_cast<uint64_t>(h) * det.W + w, vis.h);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if ((threadIdx.x & 31) == 0) atomicAdd(sig + b, static_cast<unsigned long long>(v));
+}
+
+// One CTA per pose: the CTA partials of the three 12-vectors in a fixed order,
+// combined with the loss kernel's coefficients into dL/dframe, then chained
+// to the pose: dL/deta (drr_pose_grad's map).  Either output may be NULL.
+// kReduceRows x 36 threads: thread (row r, sum k) adds tiles r, r + 8, ... of
+// sum k (consecutive threads read consecutive doubles: coalesced), then the 8
+// row totals are added in row order.  A single pose split over K lanes per ray
+// has ~1250 small tiles; this keeps its reduction off the latency path.
+constexpr int kReduceRows = 8;
+constexpr int kReduceLossThreads = kReduceRows * kLossSums;  // 288
+__global__ void __launch_bounds__(kReduceLossThreads)
+    k_reduce_loss_grad(const double* __restrict__ partials, int blocks_per_pose,
+                       const double* __restrict__ coef, const double* __restrict__ eta,
+                       double* __restrict__ grad_frames, double* __restrict__ grad_eta) {
+  const int b = blockIdx.x;
+  const int k = threadIdx.x % kLossSums, r = threadIdx.x / kLossSums;
+  __shared__ double sm[kReduceRows][kLossSums];
+  __shared__ double gf[kFrameGrads];
+  const double* base = partials + static_cast<size_t>(b) * blocks_per_pose * kLossSums + k;
+  double v0 = 0.0, v1 = 0.0;  // tiles r + 16 i and r + 8 + 16 i: two independent chains
+  int j = r;
+  for (; j + kReduceRows < blocks_per_pose; j += 2 * kReduceRows) {
+    v0 += base[static_cast<size_t>(j) * kLossSums];
+    v1 += base[static_cast<size_t>(j + kReduceRows) * kLossSums];
+  }
+  if (j < blocks_per_pose) v0 += base[static_cast<size_t>(j) * kLossSums];
+  sm[r][k] = v0 + v1;
+  __syncthreads();
+  if (threadIdx.x < kLossSums) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kReduceRows; ++q) t += sm[q][threadIdx.x];
+    sm[0][threadIdx.x] = t;  // row 0 is read again only after the barrier below
+  }
+  __syncthreads();
+  if (threadIdx.x < kFrameGrads) {
+    const int c = threadIdx.x;
+    const double c0 = coef[3 * b], c1 = coef[3 * b + 1], c2 = coef[3 * b + 2];
+    const double gk = (c0 * sm[0][c] + c1 * sm[0][kFrameGrads + c]) + c2 * sm[0][2 * kFrameGrads + c];
+    gf[c] = gk;
+    if (grad_frames) grad_frames[b * kFrameGrads + c] = gk;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && grad_eta) {
+    double ge[7];
+    pose_grad(eta + 7 * b, gf, ge);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) grad_eta[7 * b + q] = ge[q];
+  }
+}
+
 // Contraction of the stored ray Jacobians with the upstream pixel gradient,
 // reduced per CTA in the same fixed order as k_backward (16 x 8 tiles, warp
 // butterflies, warps in index order), then k_reduce_frames.
@@ -1000,6 +1204,127 @@ int drr_backward(const void* d_vol, int vol_dtype, const drr_grid* grid,
   return check_launch("drr_backward/reduce");
 }
 
+size_t drr_loss_grad_workspace_size(int32_t n_poses, const drr_detector* det) {
+  drr::DetDev d;
+  if (make_det(det, d) || n_poses < 0) return 0;
+  const dim3 grd = pose_grid(d, 1, ray_split(d, n_poses));
+  return static_cast<size_t>(n_poses) *
+         (static_cast<size_t>(grd.x) * grd.y * drr::kLossSums + 3) * sizeof(double);
+}
+
+int drr_forward_loss_grad(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                          const double* d_frames, const double* d_eta, int32_t n_poses,
+                          const drr_detector* det, const void* d_fixed, int64_t fixed_stride,
+                          int kind, void* d_img, int img_dtype, double* d_value, int* d_status,
+                          double* d_grad_frames, double* d_grad_eta, void* d_workspace,
+                          size_t workspace_bytes, void* stream) {
+  drr::GridDev g;
+  drr::DetDev d;
+  int rc = make_grid(grid, g);
+  if (rc) return rc;
+  const size_t smem = table_bytes(g, true);
+  rc = make_det(det, d);
+  if (rc) return rc;
+  if (n_poses < 0 || n_poses > 65535)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
+  if (n_poses == 0) return DRR_OK;
+  if (kind != DRR_LOSS_NEG_ZNCC && kind != DRR_LOSS_L2)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "loss kind must be neg_zncc (0) or l2 (1), got %d", kind);
+  const int64_t npix = static_cast<int64_t>(d.H) * d.W;
+  if (fixed_stride != 0 && fixed_stride != npix)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "fixed_stride must be 0 or H*W");
+  if (d_img == nullptr || d_fixed == nullptr || d_value == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "d_img, d_fixed and d_value must not be NULL");
+  if (d_grad_eta != nullptr && d_eta == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "d_grad_eta needs d_eta");
+  if ((vol_dtype != DRR_VOL_F32 && vol_dtype != DRR_VOL_F64) || (img_dtype != 0 && img_dtype != 1))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "bad dtypes vol=%d img=%d", vol_dtype, img_dtype);
+  const size_t need = drr_loss_grad_workspace_size(n_poses, det);
+  if (workspace_bytes < need || d_workspace == nullptr)
+    return fail(DRR_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int K = ray_split(d, n_poses);
+  const dim3 grd = pose_grid(d, n_poses, K);
+  const int tiles = static_cast<int>(grd.x * grd.y);
+  double* partials = static_cast<double*>(d_workspace);
+  double* coef = partials + static_cast<size_t>(n_poses) * tiles * drr::kLossSums;
+  DRR_DISPATCH_K(K,
+    if (vol_dtype == DRR_VOL_F32 && img_dtype == 0) {
+      ensure_smem(drr::k_forward_loss<float, float, kK>, smem);
+      drr::k_forward_loss<float, float, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const float*>(d_vol), g, d_frames, d, static_cast<float*>(d_img),
+          static_cast<const float*>(d_fixed), fixed_stride, partials);
+    } else if (vol_dtype == DRR_VOL_F32) {
+      ensure_smem(drr::k_forward_loss<float, double, kK>, smem);
+      drr::k_forward_loss<float, double, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const float*>(d_vol), g, d_frames, d, static_cast<double*>(d_img),
+          static_cast<const double*>(d_fixed), fixed_stride, partials);
+    } else if (img_dtype == 1) {
+      ensure_smem(drr::k_forward_loss<double, double, kK>, smem);
+      drr::k_forward_loss<double, double, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const double*>(d_vol), g, d_frames, d, static_cast<double*>(d_img),
+          static_cast<const double*>(d_fixed), fixed_stride, partials);
+    } else {
+      ensure_smem(drr::k_forward_loss<double, float, kK>, smem);
+      drr::k_forward_loss<double, float, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const double*>(d_vol), g, d_frames, d, static_cast<float*>(d_img),
+          static_cast<const float*>(d_fixed), fixed_stride, partials);
+    })
+  rc = check_launch("drr_forward_loss_grad/walk");
+  if (rc) return rc;
+  for (int32_t i0 = 0; i0 < n_poses; i0 += 65535) {
+    const int32_t n = n_poses - i0 < 65535 ? n_poses - i0 : 65535;
+    const dim3 lg(drr::kLossCluster, n);
+    const int64_t fo = fixed_stride * i0, io = npix * i0;
+    int* sts = d_status ? d_status + i0 : nullptr;
+    if (img_dtype == 0)
+      drr::k_image_loss<float><<<lg, drr::kLossThreads, 0, st>>>(
+          static_cast<const float*>(d_img) + io, static_cast<const float*>(d_fixed) + fo,
+          fixed_stride, npix, kind, d_value + i0, nullptr, sts, coef + 3 * i0);
+    else
+      drr::k_image_loss<double><<<lg, drr::kLossThreads, 0, st>>>(
+          static_cast<const double*>(d_img) + io, static_cast<const double*>(d_fixed) + fo,
+          fixed_stride, npix, kind, d_value + i0, nullptr, sts, coef + 3 * i0);
+    rc = check_launch("drr_forward_loss_grad/loss");
+    if (rc) return rc;
+  }
+  if (d_grad_frames == nullptr && d_grad_eta == nullptr) return DRR_OK;
+  drr::k_reduce_loss_grad<<<n_poses, drr::kReduceLossThreads, 0, st>>>(
+      partials, tiles, coef, d_eta, d_grad_frames, d_grad_eta);
+  return check_launch("drr_forward_loss_grad/reduce");
+}
+
+int drr_signature(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                  const double* d_frames, int32_t n_poses, const drr_detector* det,
+                  uint64_t* d_sig, void* stream) {
+  drr::GridDev g;
+  drr::DetDev d;
+  int rc = make_grid(grid, g);
+  if (rc) return rc;
+  const size_t smem = table_bytes(g, false);
+  rc = make_det(det, d);
+  if (rc) return rc;
+  if (n_poses < 0 || n_poses > 65535)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
+  if (n_poses == 0) return DRR_OK;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(d_sig, 0, sizeof(uint64_t) * n_poses, st);
+  const dim3 grd = pose_grid(d, n_poses, 1);
+  auto* out = reinterpret_cast<unsigned long long*>(d_sig);
+  if (vol_dtype == DRR_VOL_F32) {
+    ensure_smem(drr::k_signature<float>, smem);
+    drr::k_signature<float><<<grd, drr::kThreads, smem, st>>>(static_cast<const float*>(d_vol), g,
+                                                              d_frames, d, out);
+  } else if (vol_dtype == DRR_VOL_F64) {
+    ensure_smem(drr::k_signature<double>, smem);
+    drr::k_signature<double><<<grd, drr::kThreads, smem, st>>>(
+        static_cast<const double*>(d_vol), g, d_frames, d, out);
+  } else {
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
+  }
+  return check_launch("drr_signature");
+}
+
 int drr_count_steps(const void* d_vol, int vol_dtype, const drr_grid* grid,
                     const double* d_frames, int32_t n_poses,
                     const drr_detector* det, int32_t* d_steps, void* stream) {
@@ -1077,11 +1402,11 @@ int drr_image_loss(const void* d_img, const void* d_fixed, int img_dtype, int64_
     if (img_dtype == 0)
       drr::k_image_loss<float><<<grd, drr::kLossThreads, 0, st>>>(
           static_cast<const float*>(d_img) + io, static_cast<const float*>(d_fixed) + fo,
-          fixed_stride, npix, kind, val, grad, sts);
+          fixed_stride, npix, kind, val, grad, sts, nullptr);
     else
       drr::k_image_loss<double><<<grd, drr::kLossThreads, 0, st>>>(
           static_cast<const double*>(d_img) + io, static_cast<const double*>(d_fixed) + fo,
-          fixed_stride, npix, kind, val, grad, sts);
+          fixed_stride, npix, kind, val, grad, sts, nullptr);
     const int rc = check_launch("drr_image_loss");
     if (rc) return rc;
   }

@@ -53,19 +53,55 @@ __device__ __forceinline__ void block_sum5(double v[5], double* sm) {
   for (int k = 0; k < 5; ++k) v[k] = sm[kLossThreads / 32 * 5 + k];
 }
 
+// Cluster-wide fixed-order total of five per-thread partials: block_sum5 in
+// each CTA, then the CTAs' totals in rank order through distributed shared
+// memory.  Every thread of the cluster returns the image's five totals.
+template <int kThreadsT>
+__device__ __forceinline__ void cluster_sum5(double v[5], double* sm) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int kTot = kThreadsT / 32 * 5, kImg = kTot + 5;
+  block_sum5(v, sm);  // this CTA's totals in sm[kTot..kTot+5)
+  cluster.sync();     // every CTA's totals are visible cluster-wide
+  if (threadIdx.x < 5) {
+    double t = 0.0;
+    for (int r = 0; r < kLossCluster; ++r) t += *cluster.map_shared_rank(sm + kTot + threadIdx.x, r);
+    sm[kImg + threadIdx.x] = t;
+  }
+  cluster.sync();     // no CTA leaves (or reuses its totals) while they are read
+#pragma unroll
+  for (int k = 0; k < 5; ++k) v[k] = sm[kImg + k];
+}
+
 // kind 0 = neg_zncc, 1 = l2.  fixed may be shared by all images (fixed_stride 0).
 // Grid (kLossCluster, images); cluster (kLossCluster, 1, 1).
+//
+// neg_zncc is two-pass like the reference (metrics.py:26-31 centres before it
+// squares): pass 1 the means, pass 2 the centred second moments over the same
+// (L1/L2-resident) chunk, so a bright image with little structure keeps its
+// digits.  sigma == 0 (MetricUndefinedError, metrics.py:29-30) is decided
+// from the data itself: an image whose pixels are all equal is undefined even
+// when its mean rounds (so its residuals are tiny but not zero) -- pass 2 also
+// counts the pixels that differ from the first one.
+//
+// Outputs (each optional but value): value[b]; status[b] = 1 where the metric
+// is undefined (value, gradient and coefficients are then NaN, as the torch
+// restatement gives); grad = the fp32 pixel gradient (metrics.py:78-90); coef
+// = the pixel gradient as an affine map of the two images,
+//   dL/da_i = coef[0] + coef[1] a_i + coef[2] b_i   (3 doubles per image),
+// which lets a walk that already holds a_i, b_i and the ray Jacobian reduce
+// the pose gradient without the per-pixel gradient ever being stored
+// (k_forward_loss + k_reduce_loss_grad).
 template <typename IT>
 __global__ void __cluster_dims__(kLossCluster, 1, 1) __launch_bounds__(kLossThreads)
     k_image_loss(const IT* __restrict__ img, const IT* __restrict__ fixed,
                  int64_t fixed_stride, int64_t npix, int kind,
                  double* __restrict__ value, float* __restrict__ grad,
-                 int* __restrict__ status) {
+                 int* __restrict__ status, double* __restrict__ coef) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   // [0, W*5): warp partials; [W*5, W*5+5): this CTA's totals; then the image's
   __shared__ double sm[(kLossThreads / 32 + 2) * 5];
-  constexpr int kTot = kLossThreads / 32 * 5, kImg = kTot + 5;
   const int b = blockIdx.y;
   const int rank = static_cast<int>(cluster.block_rank());
   const int64_t chunk = (npix + kLossCluster - 1) / kLossCluster;
@@ -73,9 +109,10 @@ __global__ void __cluster_dims__(kLossCluster, 1, 1) __launch_bounds__(kLossThre
   const IT* a = img + static_cast<int64_t>(b) * npix;
   const IT* f = fixed + static_cast<int64_t>(b) * fixed_stride;
   float* g = grad ? grad + static_cast<int64_t>(b) * npix : nullptr;
+  const double N = static_cast<double>(npix);
   double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  // each thread sums its pixels lo + tid, lo + tid + T, ... in that order; the
-  // loads of kLossBatch of them are issued before any is summed
+  // pass 1: each thread sums its pixels lo + tid, lo + tid + T, ... in that
+  // order; the loads of kLossBatch of them are issued before any is summed
   for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += kLossThreads * kLossBatch) {
     IT xa[kLossBatch], ya[kLossBatch];
 #pragma unroll
@@ -89,37 +126,54 @@ __global__ void __cluster_dims__(kLossCluster, 1, 1) __launch_bounds__(kLossThre
       if (i0 + static_cast<int64_t>(j) * kLossThreads >= hi) break;
       const double x = static_cast<double>(xa[j]), y = static_cast<double>(ya[j]);
       if (kind == 0) {
-        v[0] += x; v[1] += x * x; v[2] += y; v[3] += y * y; v[4] += x * y;
+        v[0] += x; v[2] += y;
       } else {
         const double dd = x - y;
         v[0] += dd * dd;
       }
     }
   }
-  block_sum5(v, sm);  // this CTA's totals in sm[kTot..kTot+5)
-  cluster.sync();     // every CTA's totals are visible cluster-wide
-  if (threadIdx.x < 5) {
-    double t = 0.0;
-    for (int r = 0; r < kLossCluster; ++r) t += *cluster.map_shared_rank(sm + kTot + threadIdx.x, r);
-    sm[kImg + threadIdx.x] = t;
-  }
-  cluster.sync();     // no CTA leaves (or reuses its totals) while they are read
-#pragma unroll
-  for (int k = 0; k < 5; ++k) v[k] = sm[kImg + k];
-  const double N = static_cast<double>(npix);
+  cluster_sum5<kLossThreads>(v, sm);
   if (kind == 0) {
     const double ma = v[0] / N, mb = v[2] / N;
-    const double va = fmax(v[1] / N - ma * ma, 0.0), vb = fmax(v[3] / N - mb * mb, 0.0);
-    const double sa = sqrt(va), sb = sqrt(vb);
-    const bool undefined = !(sa > 0.0) || !(sb > 0.0);
-    const double raw = undefined ? 0.0 : (v[4] / N - ma * mb) / (sa * sb);
+    const double a0 = static_cast<double>(a[0]), b0 = static_cast<double>(f[0]);
+    // pass 2: centred moments and the count of pixels unlike the first
+    double w[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += kLossThreads * kLossBatch) {
+      IT xa[kLossBatch], ya[kLossBatch];
+#pragma unroll
+      for (int j = 0; j < kLossBatch; ++j) {
+        const int64_t i = i0 + static_cast<int64_t>(j) * kLossThreads;
+        xa[j] = i < hi ? a[i] : IT(0);
+        ya[j] = i < hi ? f[i] : IT(0);
+      }
+#pragma unroll
+      for (int j = 0; j < kLossBatch; ++j) {
+        if (i0 + static_cast<int64_t>(j) * kLossThreads >= hi) break;
+        const double x = static_cast<double>(xa[j]), y = static_cast<double>(ya[j]);
+        const double dx = x - ma, dy = y - mb;
+        w[0] += dx * dx; w[1] += dy * dy; w[2] += dx * dy;
+        w[3] += x != a0 ? 1.0 : 0.0;
+        w[4] += y != b0 ? 1.0 : 0.0;
+      }
+    }
+    cluster_sum5<kLossThreads>(w, sm);
+    const double sa = sqrt(w[0] / N), sb = sqrt(w[1] / N);
+    const bool undefined = w[3] == 0.0 || w[4] == 0.0 || !(sa > 0.0) || !(sb > 0.0);
+    const double raw = undefined ? NAN : w[2] / (N * sa * sb);
+    const double scale = undefined ? NAN : -1.0 / (N * sa);
     if (rank == 0 && threadIdx.x == 0) {
       value[b] = undefined ? NAN : -fmin(1.0, fmax(-1.0, raw));
       if (status) status[b] = undefined ? 1 : 0;
+      if (coef) {
+        // scale (bh - raw ah) with ah = (a - ma)/sa, bh = (b - mb)/sb
+        coef[3 * b + 0] = scale * (raw * ma / sa - mb / sb);
+        coef[3 * b + 1] = -scale * raw / sa;
+        coef[3 * b + 2] = scale / sb;
+      }
     }
     if (g) {
-      const double inv_sa = undefined ? 0.0 : 1.0 / sa, inv_sb = undefined ? 0.0 : 1.0 / sb;
-      const double scale = undefined ? 0.0 : -1.0 / (N * sa);
+      const double inv_sa = 1.0 / sa, inv_sb = 1.0 / sb;
 #pragma unroll 4
       for (int64_t i = lo + threadIdx.x; i < hi; i += kLossThreads) {
         const double ah = (static_cast<double>(a[i]) - ma) * inv_sa;
@@ -129,12 +183,17 @@ __global__ void __cluster_dims__(kLossCluster, 1, 1) __launch_bounds__(kLossThre
     }
   } else {
     const double norm = sqrt(v[0]);
+    const double inv = norm > 0.0 ? 1.0 / norm : 0.0;
     if (rank == 0 && threadIdx.x == 0) {
       value[b] = norm;
       if (status) status[b] = 0;
+      if (coef) {
+        coef[3 * b + 0] = 0.0;
+        coef[3 * b + 1] = inv;
+        coef[3 * b + 2] = -inv;
+      }
     }
     if (g) {
-      const double inv = norm > 0.0 ? 1.0 / norm : 0.0;
 #pragma unroll 4
       for (int64_t i = lo + threadIdx.x; i < hi; i += kLossThreads)
         g[i] = static_cast<float>((static_cast<double>(a[i]) - static_cast<double>(f[i])) * inv);

@@ -398,6 +398,7 @@ __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
       idx = exact_voxel(g, s0, s1, s2, d0, d1, d2, 0.5 * (prev + cur));
     VT v = VT(0);
     if (used) v = __ldg(vol + idx);
+    if constexpr (Visitor::kIndex) vis.index(used, idx, lab);
     vis.segment(pipe[0].used, pipe[0].seg, static_cast<double>(pipe[0].v), pipe[0].lab,
                 pipe[0].a);
 #pragma unroll
@@ -430,6 +431,7 @@ __device__ __forceinline__ void walk_select(const VT* __restrict__ vol,
 // ---- visitors ----------------------------------------------------------
 
 struct SumVisitor {
+  static constexpr bool kIndex = false;
   double acc = 0.0;
   __device__ __forceinline__ void segment(bool used, double seg, double v, int,
                                           double) {
@@ -442,6 +444,7 @@ struct SumVisitor {
 };
 
 struct CountVisitor {
+  static constexpr bool kIndex = false;
   int steps = 0;
   __device__ __forceinline__ void segment(bool used, double, double, int, double) {
     steps += used ? 1 : 0;
@@ -455,6 +458,7 @@ struct CountVisitor {
 // d alpha_k/dp_a = -alpha_k/d_a the ray's endpoint gradients need only
 // G_a = sum c_k and H_a = sum c_k alpha_k.  Label 3 (clip) has no tangent.
 struct GradVisitor {
+  static constexpr bool kIndex = false;
   double acc = 0.0;
   double pend = 0.0;  // value of the used segment ending at the next crossing
   double G0 = 0.0, G1 = 0.0, G2 = 0.0, H0 = 0.0, H1 = 0.0, H2 = 0.0;
@@ -478,6 +482,30 @@ struct GradVisitor {
   }
   __device__ __forceinline__ void finish(int lab_end, double a_end) {
     apply(lab_end, a_end, pend);
+  }
+};
+
+// Discrete structure of a traversal (python_ref.py:191-201 ray_structure:
+// crossing labels in merge order, the used set, the voxel of each used
+// segment, the exit selector) folded into a 64-bit hash.  Two poses whose
+// rays hash alike share the piecewise-smooth branch of the energy map, so a
+// finite-difference stencil between them is kink-free (gradients.py:124-167).
+__host__ __device__ __forceinline__ uint64_t sig_mix(uint64_t h, uint64_t x) {
+  h ^= x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+  h ^= h >> 29;
+  h *= 0xBF58476D1CE4E5B9ull;
+  return h ^ (h >> 32);
+}
+struct SigVisitor {
+  static constexpr bool kIndex = true;
+  uint64_t h = 0x6A09E667F3BCC908ull;
+  __device__ __forceinline__ void index(bool used, int idx, int lab) {
+    h = sig_mix(h, (static_cast<uint64_t>(used ? static_cast<uint32_t>(idx) : 0xFFFFFFFFu) << 8) |
+                       static_cast<uint64_t>(lab & 0xFF));
+  }
+  __device__ __forceinline__ void segment(bool, double, double, int, double) {}
+  __device__ __forceinline__ void finish(int lab_end, double) {
+    h = sig_mix(h, 0x100u | static_cast<uint64_t>(lab_end & 0xFF));
   }
 };
 

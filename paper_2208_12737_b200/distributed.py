@@ -307,7 +307,7 @@ class ShardedDRR:
         """Batched ``gradients.loss_and_gradient`` (``gradients.py:61-69``) over
         the global pose batch: (value (n,), grad (n, 7)) on ``dst``.  Each rank
         runs the native chain on its shard; the loss kernel stores the values
-        and the pose-gradient kernel the gradients straight into ``dst``'s
+        and the reduction kernel the gradients straight into ``dst``'s
         buffers."""
         from .registration import LOSS_KINDS, _launch_loss_grad, _prep_fixed, _Buffers, _iso
         n, lo, e = self._local_eta(eta)
@@ -332,9 +332,8 @@ class ShardedDRR:
             st = torch.cuda.current_stream(self.device).cuda_stream
             _launch_loss_grad(lib, self.volume, self.detector, _iso(self.volume, None), e,
                               fixed_t, stride, LOSS_KINDS[loss_kind], buf, st,
-                              value_ptr=vals.ptr(lo))
-            _lib.check(lib.drr_pose_grad(e.data_ptr(), buf.grad_frames.data_ptr(), b,
-                                         grads.ptr(lo), st))
+                              value_ptr=vals.ptr(lo), grad_eta_ptr=grads.ptr(lo),
+                              grad_frames=False)
         return self._finish((vals.rows(), grads.rows()), copy)
 
     def register_batch(self, fixed_images, poses0, config=None, use_graph: bool = True):

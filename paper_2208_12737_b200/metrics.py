@@ -5,11 +5,13 @@ reference, ``pkg/src/drrtrace/metrics.py:26-91``).
 clips the correlation to [-1, 1] (``metrics.py:48-49``); its analytic pixel
 gradient is -(b_hat - raw a_hat) / (N sigma_a) (``metrics.py:78-84``).
 
-On the device, for float32 moving images, both losses run as one fused kernel
-(``drr_image_loss``: value and the reference's analytic pixel gradient,
-``loss_value_and_pixel_grad``) wrapped in an autograd Function; elsewhere
-(host tensors, float64 images, a fixed image that requires grad) they are
-plain differentiable torch with the same value.
+On the device, for float32 moving AND fixed images, both losses run as one
+fused kernel (``drr_image_loss``: value and the reference's analytic pixel
+gradient, ``loss_value_and_pixel_grad``) wrapped in an autograd Function;
+elsewhere (host tensors, float64 images -- which the kernel would otherwise
+round -- a fixed image that requires grad) they are plain differentiable torch
+with the same value.  An undefined ZNCC (a constant image, metrics.py:29-30)
+gives NaN value and NaN gradient on both paths.
 """
 
 from __future__ import annotations
@@ -37,7 +39,7 @@ class _ImageLoss(torch.autograd.Function):
         single = moving.ndim == 2
         m = moving.detach().reshape(-1, *moving.shape[-2:]).contiguous()
         B, npix = m.shape[0], m.shape[-2] * m.shape[-1]
-        f = fixed.detach().to(device=m.device, dtype=torch.float32)
+        f = fixed.detach()
         if f.ndim == 3 and f.shape[0] == 1:
             f = f[0]
         if f.ndim == 3 and f.shape[0] != B:
@@ -67,6 +69,8 @@ def _fused_ok(moving: torch.Tensor, fixed: torch.Tensor) -> bool:
     if not (moving.is_cuda and moving.dtype == torch.float32 and moving.ndim in (2, 3)):
         return False
     if not isinstance(fixed, torch.Tensor) or fixed.requires_grad:
+        return False
+    if fixed.dtype != torch.float32 or fixed.device != moving.device:
         return False
     B = moving.shape[0] if moving.ndim == 3 else 1
     return fixed.ndim == 2 or (fixed.ndim == 3 and fixed.shape[0] in (1, B) and moving.ndim == 3)

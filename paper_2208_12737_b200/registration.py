@@ -3,17 +3,23 @@
 Mirrors the reference's ``gradients.loss_and_gradient`` (``gradients.py:61-69``)
 and ``registration.register`` (``registration.py:89-125``), batched:
 
-* :func:`loss_and_gradient` -- B poses at once: ``drr_pose_frames`` ->
-  ``drr_forward_jac`` (image + per-ray Jacobian from one walk of each ray) ->
-  ``drr_image_loss`` (fused neg-ZNCC / L2 value + pixel gradient) ->
-  ``drr_backward_jac`` (walk-free contraction) -> ``drr_pose_grad``.  Native
-  launches only, no host round trip, no torch autograd.
+* :func:`loss_and_gradient` -- B poses at once: ``drr_pose_frames`` -> one
+  walk per ray -> the fused neg-ZNCC / L2 value and pixel gradient -> dL/dframe
+  -> dL/deta, as native launches only (no host round trip, no torch
+  autograd).  Two chains (:class:`_Buffers`): the stored ray Jacobian and its
+  contraction (``drr_forward_jac`` / ``drr_image_loss`` /
+  ``drr_backward_jac``), or ``drr_forward_loss_grad`` (no Jacobian: per-CTA
+  sums of the ray Jacobian weighted by 1, the image and the fixed image,
+  combined with the loss kernel's affine pixel-gradient coefficients).
 * :class:`RegistrationEngine` -- B independent momentum-GD registrations
   (``OptimizerConfig`` defaults = the paper's hyper-parameters,
-  ``registration.py:41-58``).  Each iteration is the five launches above plus
+  ``registration.py:41-58``).  Each iteration is the chain above plus
   ``drr_register_update``, which keeps the reference's convergence / failure
   bookkeeping on the device; the whole ``max_iters + 1`` loop is captured in
   one CUDA graph.
+
+Images are float32 by default (the product path); ``image_dtype=torch.float64``
+renders and scores in float64 as the reference does (``api.register``).
 """
 
 from __future__ import annotations
@@ -53,13 +59,20 @@ class OptimizerConfig:
             raise InvalidArgumentError(f"loss kind must be one of {tuple(LOSS_KINDS)}")
 
     def c(self):
-        cfg = _lib.DrrRegConfig()
-        cfg.lr_rotation = self.lr_rotation
-        cfg.lr_translation = self.lr_translation
-        cfg.momentum = self.momentum
-        cfg.converged_threshold = self.converged_threshold
-        cfg.max_iters = self.max_iters
-        return cfg
+        return reg_config_c(self)
+
+
+def reg_config_c(config) -> "_lib.DrrRegConfig":
+    """The C-ABI settings from any config with the reference's fields
+    (``registration.py:41-58``): this module's OptimizerConfig or the
+    reference's own (duck-typed, no method needed)."""
+    cfg = _lib.DrrRegConfig()
+    cfg.lr_rotation = float(config.lr_rotation)
+    cfg.lr_translation = float(config.lr_translation)
+    cfg.momentum = float(config.momentum)
+    cfg.converged_threshold = float(config.converged_threshold)
+    cfg.max_iters = int(config.max_iters)
+    return cfg
 
 
 @dataclass
@@ -80,40 +93,82 @@ class RegistrationTrace:
     def final_loss(self) -> float:
         return float(self.losses[-1])
 
+    def final_pose(self):
+        """registration.py:84-85: the last recorded pose with the fixed rho."""
+        from .api import PoseParameters
+        return PoseParameters.from_vector(np.concatenate([[self.rho], self.poses[-1]]))
+
 
 def _stream(dev) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 
 
 class _Buffers:
-    """Device buffers for B poses; reused across calls (no allocation in the loop)."""
+    """Device buffers for B poses; reused across calls (no allocation in the loop).
 
-    def __init__(self, vol: DeviceVolume, det: Detector, B: int):
+    Two native chains compute the same step (``mode``):
+
+    * ``"jac"`` -- ``drr_forward_jac`` stores each ray's 6-double Jacobian
+      (48 B/pixel), ``drr_image_loss`` writes the pixel gradient and
+      ``drr_backward_jac`` contracts the two: measured ~3% faster at C2 (the
+      fused walk's per-CTA 36-sum epilogue costs more than the stored
+      contraction; profiles/r02/SUMMARY.md);
+    * ``"fused"`` -- ``drr_forward_loss_grad``: no Jacobian, the pixel gradient
+      as an affine map of the two images reduced inside the walk; float64
+      pixel gradients (used for float64 images) and any batch size.
+
+    ``"auto"`` takes ``"jac"`` for float32 images whose Jacobian fits
+    ``renderer.JAC_BUDGET_BYTES`` (C2: 256 poses = 0.5 GB), else ``"fused"``
+    (C5: 64 poses at 1024^2 would hold 3.2 GB)."""
+
+    def __init__(self, vol: DeviceVolume, det: Detector, B: int, image_dtype=torch.float32,
+                 mode: str = "auto"):
+        from .renderer import JAC_BUDGET_BYTES, jac_bytes
         dev = vol.device
+        if mode not in ("auto", "jac", "fused"):
+            raise InvalidArgumentError(f"mode must be 'auto', 'jac' or 'fused', got {mode!r}")
+        if mode == "auto":
+            mode = ("jac" if image_dtype == torch.float32 and jac_bytes(det, B) <= JAC_BUDGET_BYTES
+                    else "fused")
+        if mode == "jac" and image_dtype != torch.float32:
+            raise InvalidArgumentError("the stored-Jacobian chain takes float32 images")
+        self.mode = mode
         self.B = B
+        self.image_dtype = image_dtype
+        self.img_code = 1 if image_dtype == torch.float64 else 0
         self.frames = torch.empty((B, 12), dtype=torch.float64, device=dev)
-        self.img = torch.empty((B, det.height, det.width), dtype=torch.float32, device=dev)
-        self.pix_grad = torch.empty_like(self.img)
+        self.img = torch.empty((B, det.height, det.width), dtype=image_dtype, device=dev)
         self.value = torch.empty(B, dtype=torch.float64, device=dev)
         self.status = torch.zeros(B, dtype=torch.int32, device=dev)
         self.grad_frames = torch.empty((B, 12), dtype=torch.float64, device=dev)
         self.grad_eta = torch.empty((B, 7), dtype=torch.float64, device=dev)
-        # per-ray Jacobian of the one-walk forward (6 float64 per pixel)
-        self.jac = torch.empty((6, B * det.height * det.width), dtype=torch.float64, device=dev)
         lib = _lib.load()
-        self.ws_bytes = lib.drr_backward_workspace_size(B, det.c)
+        if mode == "jac":
+            self.jac = torch.empty((6, B * det.height * det.width), dtype=torch.float64, device=dev)
+            self.pix_grad = torch.empty((B, det.height, det.width), dtype=torch.float32,
+                                        device=dev)
+            self.ws_bytes = lib.drr_backward_workspace_size(B, det.c)
+        else:
+            self.ws_bytes = lib.drr_loss_grad_workspace_size(B, det.c)
         self.ws = torch.empty(max(self.ws_bytes, 8), dtype=torch.uint8, device=dev)
 
 
 def _launch_loss_grad(lib, vol, det, iso, eta, fixed, fixed_stride, kind, buf, stream,
-                      value_ptr=None):
-    """pose frames -> forward + ray Jacobian -> loss value and pixel gradient ->
-    contraction to dL/dframe (buf.grad_frames).  The loss values go to
-    ``value_ptr`` when given (e.g. another rank's buffer, distributed.PeerRows),
-    else to buf.value."""
+                      value_ptr=None, grad_eta_ptr=None, grad_frames=True):
+    """pose frames -> one walk per ray -> loss value + pixel gradient -> dL/dframe
+    (buf.grad_frames) -> dL/deta (``grad_eta_ptr``, when given); the loss values
+    go to ``value_ptr`` (or buf.value).  The output pointers may be another
+    rank's buffers (distributed.PeerRows).  ``buf.mode`` picks the chain."""
     B = buf.B
     value_ptr = buf.value.data_ptr() if value_ptr is None else value_ptr
     _lib.check(lib.drr_pose_frames(eta.data_ptr(), B, iso, buf.frames.data_ptr(), stream))
+    if buf.mode == "fused":
+        _lib.check(lib.drr_forward_loss_grad(
+            vol.flat.data_ptr(), vol.vol_dtype, vol.grid, buf.frames.data_ptr(), eta.data_ptr(),
+            B, det.c, fixed.data_ptr(), fixed_stride, kind, buf.img.data_ptr(), buf.img_code,
+            value_ptr, buf.status.data_ptr(), buf.grad_frames.data_ptr() if grad_frames else None,
+            grad_eta_ptr, buf.ws.data_ptr(), buf.ws_bytes, stream))
+        return
     _lib.check(lib.drr_forward_jac(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
                                    buf.frames.data_ptr(), B, det.c, buf.img.data_ptr(), 0,
                                    buf.jac.data_ptr(), stream))
@@ -123,10 +178,15 @@ def _launch_loss_grad(lib, vol, det, iso, eta, fixed, fixed_stride, kind, buf, s
     _lib.check(lib.drr_backward_jac(buf.jac.data_ptr(), B, det.c, buf.pix_grad.data_ptr(), 0,
                                     buf.grad_frames.data_ptr(), buf.ws.data_ptr(),
                                     buf.ws_bytes, stream))
+    if grad_eta_ptr is not None:
+        _lib.check(lib.drr_pose_grad(eta.data_ptr(), buf.grad_frames.data_ptr(), B,
+                                     grad_eta_ptr, stream))
 
 
-def _prep_fixed(fixed, B, det, dev):
-    fixed = torch.as_tensor(fixed, device=dev, dtype=torch.float32)
+def _prep_fixed(fixed, B, det, dev, dtype=torch.float32):
+    if not isinstance(fixed, (torch.Tensor, np.ndarray)) and hasattr(fixed, "values"):
+        fixed = fixed.values  # a reference Image
+    fixed = torch.as_tensor(fixed, device=dev, dtype=dtype)
     if fixed.shape[-2:] != (det.height, det.width):
         raise InvalidArgumentError(
             f"fixed image shape {tuple(fixed.shape)} does not match detector {det.height}x{det.width}")
@@ -138,7 +198,8 @@ def _prep_fixed(fixed, B, det, dev):
 
 
 def loss_and_gradient(vol: DeviceVolume, det: Detector, eta, fixed, loss_kind: str = "neg_zncc",
-                      isocenter=None, buffers: _Buffers | None = None):
+                      isocenter=None, buffers: _Buffers | None = None,
+                      image_dtype=torch.float32, mode: str = "auto"):
     """Batched ``gradients.loss_and_gradient``: (value (B,), grad (B, 7)) for
     pose vectors eta (B, 7) = (rho, theta, phi, gamma, bx, by, bz).
 
@@ -152,14 +213,14 @@ def loss_and_gradient(vol: DeviceVolume, det: Detector, eta, fixed, loss_kind: s
         eta = eta[None]
     eta = eta.contiguous()
     B = eta.shape[0]
-    buf = buffers if buffers is not None and buffers.B == B else _Buffers(vol, det, B)
-    fixed_t, stride = _prep_fixed(fixed, B, det, dev)
+    buf = (buffers if buffers is not None and buffers.B == B
+           and buffers.image_dtype == image_dtype else _Buffers(vol, det, B, image_dtype, mode))
+    fixed_t, stride = _prep_fixed(fixed, B, det, dev, image_dtype)
     iso = _iso(vol, isocenter)
     lib = _lib.load()
     st = _stream(dev)
-    _launch_loss_grad(lib, vol, det, iso, eta, fixed_t, stride, LOSS_KINDS[loss_kind], buf, st)
-    _lib.check(lib.drr_pose_grad(eta.data_ptr(), buf.grad_frames.data_ptr(), B,
-                                 buf.grad_eta.data_ptr(), st))
+    _launch_loss_grad(lib, vol, det, iso, eta, fixed_t, stride, LOSS_KINDS[loss_kind], buf, st,
+                      grad_eta_ptr=buf.grad_eta.data_ptr(), grad_frames=False)
     return buf.value.clone(), buf.grad_eta.clone()
 
 
@@ -173,13 +234,14 @@ class RegistrationEngine:
     """B independent registrations of fixed image(s) against one CT volume."""
 
     def __init__(self, vol: DeviceVolume, det: Detector, fixed, B: int = 1,
-                 config: OptimizerConfig | None = None, isocenter=None):
+                 config: OptimizerConfig | None = None, isocenter=None,
+                 image_dtype=torch.float32, mode: str = "auto"):
         self.vol, self.det, self.B = vol, det, int(B)
         self.config = config or OptimizerConfig()
         dev = vol.device
-        self.fixed, self.fixed_stride = _prep_fixed(fixed, self.B, det, dev)
+        self.fixed, self.fixed_stride = _prep_fixed(fixed, self.B, det, dev, image_dtype)
         self.iso = _iso(vol, isocenter)
-        self.buf = _Buffers(vol, det, self.B)
+        self.buf = _Buffers(vol, det, self.B, image_dtype, mode)
         T = self.config.max_iters + 1
         self.eta = torch.zeros((self.B, 7), dtype=torch.float64, device=dev)
         self.vel = torch.zeros((self.B, 6), dtype=torch.float64, device=dev)
@@ -188,8 +250,11 @@ class RegistrationEngine:
         self.trace_eta = torch.zeros((self.B, T, 6), dtype=torch.float64, device=dev)
         self.trace_loss = torch.zeros((self.B, T), dtype=torch.float64, device=dev)
         self.graph = None
-        self.kind = LOSS_KINDS[self.config.loss_kind]
-        self._cfg = self.config.c()
+        kind = getattr(self.config, "loss_kind", "neg_zncc")
+        if kind not in LOSS_KINDS:
+            raise InvalidArgumentError(f"loss kind must be one of {tuple(LOSS_KINDS)}, got {kind!r}")
+        self.kind = LOSS_KINDS[kind]
+        self._cfg = reg_config_c(self.config)
 
     def reset(self, poses0):
         p = torch.as_tensor(poses0, dtype=torch.float64, device=self.vol.device).reshape(self.B, 7)

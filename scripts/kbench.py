@@ -27,7 +27,21 @@ for B in [int(x) for x in (sys.argv[1:] or ["32", "1"])]:
     frames = pose_frames(torch.tensor(poses, device=dev), drr.isocenter)
     S = float(count_steps(drr.volume, drr.detector, frames).double().sum())
     g = torch.randn((B, 200, 200), device=dev)
-    fns = {"fwd": lambda: render_frames(drr.volume, drr.detector, frames),
+    from paper_2208_12737_b200 import _lib
+    from paper_2208_12737_b200.registration import _Buffers
+    lib = _lib.load()
+    lb = _Buffers(drr.volume, drr.detector, B)
+    et = torch.tensor(poses, device=dev)
+    fixed = torch.rand((200, 200), device=dev)
+
+    def fused():
+        _lib.check(lib.drr_forward_loss_grad(
+            drr.volume.flat.data_ptr(), 0, drr.volume.grid, frames.data_ptr(), et.data_ptr(), B,
+            drr.detector.c, fixed.data_ptr(), 0, 0, lb.img.data_ptr(), 0, lb.value.data_ptr(),
+            lb.status.data_ptr(), lb.grad_frames.data_ptr(), lb.grad_eta.data_ptr(),
+            lb.ws.data_ptr(), lb.ws_bytes, torch.cuda.current_stream().cuda_stream))
+    fns = {"fl": fused,
+           "fwd": lambda: render_frames(drr.volume, drr.detector, frames),
            "bwd": lambda: backward_frames(drr.volume, drr.detector, frames, g),
            "fj": lambda: hold.__setitem__(0, render_frames_jac(drr.volume, drr.detector, frames)[1]),
            "bj": lambda: backward_from_jac(drr.detector, hold[0], g)}
@@ -41,7 +55,7 @@ for B in [int(x) for x in (sys.argv[1:] or ["32", "1"])]:
             if i >= 2:
                 t[k].append(a.elapsed_time(b))
     m = {k: float(np.median(v)) for k, v in t.items()}
-    res[B] = {"fwd_ms": m["fwd"], "bwd_ms": m["bwd"], "fwd_jac_ms": m["fj"], "bwd_jac_ms": m["bj"],
+    res[B] = {"fused_loss_ms": m["fl"], "fwd_ms": m["fwd"], "bwd_ms": m["bwd"], "fwd_jac_ms": m["fj"], "bwd_jac_ms": m["bj"],
               "steps_per_drr": S / B,
               "fwd_gsteps_s": S / m["fwd"] / 1e6, "fwd_jac_gsteps_s": S / m["fj"] / 1e6,
               "rewalk_drr_s": B / ((m["fwd"] + m["bwd"]) / 1e3),

@@ -10,3 +10,6 @@ template __global__ void drr::k_forward<float, float, 1>(const float*, const drr
 template __global__ void drr::k_backward<float, float, float, 1>(const float*, const drr::GridDev,
                                                                  const double*, const drr::DetDev,
                                                                  const float*, float*, double*);
+template __global__ void drr::k_forward_loss<float, float, 1>(const float*, const drr::GridDev,
+                                                              const double*, const drr::DetDev,
+                                                              float*, const float*, int64_t, double*);

@@ -35,7 +35,7 @@ def test_criterion_6_registration_population(blob, cuda_device):
     from paper_2208_12737_b200 import Detector, pose_frames, render_frames, synthetic
     from paper_2208_12737_b200.registration import OptimizerConfig, register_batch
     det = Detector(100, 100, 4.0)
-    f = pose_frames(torch.tensor([TRUTH], device=cuda_device), blob.center).detach()
+    f = pose_frames(torch.tensor([TRUTH], dtype=torch.float64, device=cuda_device), blob.center).detach()
     fixed = render_frames(blob, det, f)[0]
     inits = synthetic.sample_poses(TRUTH, WIDE_HALF_WIDTHS, 50, seed=0)
     cfg = OptimizerConfig()
@@ -51,7 +51,7 @@ def test_criterion_6_registration_population(blob, cuda_device):
 def test_criterion_7_performance_scaling(blob, cuda_device):
     from paper_2208_12737_b200 import (Detector, backward_from_jac, pose_frames, render_frames,
                                        render_frames_jac)
-    f = pose_frames(torch.tensor([TRUTH], device=cuda_device), blob.center).detach()
+    f = pose_frames(torch.tensor([TRUTH], dtype=torch.float64, device=cuda_device), blob.center).detach()
 
     def timed(fn, reps=20):
         fn()
