@@ -42,6 +42,9 @@
  *                               walk per ray, no stored Jacobian
  *   drr_register_update      <- one iteration of registration.py:89-125
  *                               register() (momentum GD + convergence state)
+ *   drr_volume_pack          <- volume.py:77-79 flat_data() (the x-fastest
+ *                               layout) + volume.py:196-222 import_raw's cast
+ *                               and clamp, as one device pass
  *   drr_peer_export / _open  <- no reference counterpart: the population
  *   / _close                    study runs independent registrations in
  *                               parallel processes and collects their traces
@@ -151,6 +154,22 @@ int drr_backward_jac(const double *d_jac, int32_t n_poses,
                      const drr_detector *det, const void *d_grad_img,
                      int grad_dtype, double *d_grad_frames, void *d_workspace,
                      size_t workspace_bytes, void *stream);
+
+/* One-time ingest of a device volume into the walk's layout: x-fastest
+ * (flat = i + nx (j + ny k), volume.py:77-79), dst_dtype DRR_VOL_F32 / F64.
+ * The source is either already x-fastest (DRR_ORDER_XFASTEST: flat_data(),
+ * .dvol and raw payloads) or a C-ordered (nx, ny, nz) array data[i, j, k]
+ * (DRR_ORDER_ZFASTEST: numpy / torch default); it is cast without rescaling
+ * and, with clamp_negative, negatives become 0. */
+#define DRR_SRC_F32 0
+#define DRR_SRC_F64 1
+#define DRR_SRC_I16 2
+#define DRR_SRC_U8 3
+#define DRR_ORDER_XFASTEST 0
+#define DRR_ORDER_ZFASTEST 1
+int drr_volume_pack(const void *d_src, int src_type, int src_order,
+                    const int64_t *dims, int clamp_negative, void *d_dst,
+                    int dst_dtype, void *stream);
 
 /* Used voxel-steps per ray (segments longer than 1e-12), B x H x W int32. */
 int drr_count_steps(const void *d_vol, int vol_dtype, const drr_grid *grid,

@@ -37,6 +37,7 @@ EXPORTS = (
     "drr_forward_jac",
     "drr_backward_jac",
     "drr_count_steps",
+    "drr_volume_pack",
     "drr_signature",
     "drr_pose_frames",
     "drr_pose_grad",
@@ -97,6 +98,7 @@ _SIGNATURES = {
     "drr_forward_jac": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp, _vp], _int),
     "drr_backward_jac": ([_vp, _i32, _DP, _vp, _int, _vp, _vp, _sz, _vp], _int),
     "drr_count_steps": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
+    "drr_volume_pack": ([_vp, _int, _int, ctypes.POINTER(_i64), _int, _vp, _int, _vp], _int),
     "drr_signature": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
     "drr_pose_frames": ([_vp, _i32, ctypes.POINTER(ctypes.c_double), _vp, _vp], _int),
     "drr_pose_grad": ([_vp, _vp, _i32, _vp, _vp], _int),
@@ -110,6 +112,9 @@ _SIGNATURES = {
     "drr_peer_open": ([ctypes.POINTER(DrrPeerHandle), ctypes.POINTER(_vp)], _int),
     "drr_peer_close": ([_vp, ctypes.c_uint64], _int),
 }
+
+DRR_SRC_F32, DRR_SRC_F64, DRR_SRC_I16, DRR_SRC_U8 = 0, 1, 2, 3
+DRR_ORDER_XFASTEST, DRR_ORDER_ZFASTEST = 0, 1
 
 DRR_LOSS_NEG_ZNCC = 0
 DRR_LOSS_L2 = 1

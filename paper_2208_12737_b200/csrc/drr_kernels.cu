@@ -31,6 +31,7 @@
 #include "siddon_lean.cuh"
 #include "loss_kernels.cuh"
 #include "pose_kernels.cuh"
+#include "volume_pack.cuh"
 
 namespace drr {
 
@@ -974,6 +975,35 @@ void launch_backward(const VT* vol, const drr::GridDev& g,
 
 }  // namespace
 
+namespace {
+template <typename ST, typename DT>
+void launch_pack(const ST* src, int order, const int64_t* dims, int clamp, DT* dst,
+                 cudaStream_t st) {
+  const int64_t n = dims[0] * dims[1] * dims[2];
+  if (order == DRR_ORDER_XFASTEST) {
+    const int64_t blocks = (n + 255) / 256;
+    drr::k_pack_linear<ST, DT><<<static_cast<unsigned>(blocks < 148 * 32 ? blocks : 148 * 32), 256,
+                                 0, st>>>(src, n, clamp, dst);
+  } else {
+    const dim3 grd(static_cast<unsigned>((dims[2] + 31) / 32),
+                   static_cast<unsigned>((dims[0] + 31) / 32), static_cast<unsigned>(dims[1]));
+    drr::k_pack_zfastest<ST, DT><<<grd, dim3(32, 8), 0, st>>>(
+        src, static_cast<int>(dims[0]), static_cast<int>(dims[1]), static_cast<int>(dims[2]),
+        clamp, dst);
+  }
+}
+template <typename DT>
+void dispatch_pack(const void* src, int src_type, int order, const int64_t* dims, int clamp,
+                   DT* dst, cudaStream_t st) {
+  switch (src_type) {
+    case DRR_SRC_F32: launch_pack(static_cast<const float*>(src), order, dims, clamp, dst, st); break;
+    case DRR_SRC_F64: launch_pack(static_cast<const double*>(src), order, dims, clamp, dst, st); break;
+    case DRR_SRC_I16: launch_pack(static_cast<const int16_t*>(src), order, dims, clamp, dst, st); break;
+    default: launch_pack(static_cast<const uint8_t*>(src), order, dims, clamp, dst, st); break;
+  }
+}
+}  // namespace
+
 extern "C" {
 
 const char* drr_last_error(void) { return g_err; }
@@ -1323,6 +1353,37 @@ int drr_signature(const void* d_vol, int vol_dtype, const drr_grid* grid,
     return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
   }
   return check_launch("drr_signature");
+}
+
+int drr_volume_pack(const void* d_src, int src_type, int src_order, const int64_t* dims,
+                    int clamp_negative, void* d_dst, int dst_dtype, void* stream) {
+  if (d_src == nullptr || d_dst == nullptr || dims == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "drr_volume_pack: NULL argument");
+  int64_t total = 1;
+  for (int a = 0; a < 3; ++a) {
+    if (dims[a] < 1)
+      return fail(DRR_ERR_INVALID_ARGUMENT, "dims must be >= 1, got %lld on axis %d",
+                  (long long)dims[a], a);
+    total *= dims[a];
+  }
+  if (total >= (int64_t(1) << 31))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "volume has %lld voxels; limit is 2^31-1",
+                (long long)total);
+  if (src_type != DRR_SRC_F32 && src_type != DRR_SRC_F64 && src_type != DRR_SRC_I16 &&
+      src_type != DRR_SRC_U8)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown source type %d", src_type);
+  if (src_order != DRR_ORDER_XFASTEST && src_order != DRR_ORDER_ZFASTEST)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown source order %d", src_order);
+  if (dims[1] > 65535 && src_order == DRR_ORDER_ZFASTEST)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "ny must be <= 65535 for a z-fastest source");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dst_dtype == DRR_VOL_F32)
+    dispatch_pack(d_src, src_type, src_order, dims, clamp_negative, static_cast<float*>(d_dst), st);
+  else if (dst_dtype == DRR_VOL_F64)
+    dispatch_pack(d_src, src_type, src_order, dims, clamp_negative, static_cast<double*>(d_dst), st);
+  else
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown dst_dtype %d", dst_dtype);
+  return check_launch("drr_volume_pack");
 }
 
 int drr_count_steps(const void* d_vol, int vol_dtype, const drr_grid* grid,

@@ -40,6 +40,31 @@ def _require_cuda(t: torch.Tensor, name: str) -> None:
         raise InvalidArgumentError(f"{name} must be a CUDA tensor (no CPU fallback)")
 
 
+_SRC_CODES = {torch.float32: _lib.DRR_SRC_F32, torch.float64: _lib.DRR_SRC_F64,
+              torch.int16: _lib.DRR_SRC_I16, torch.uint8: _lib.DRR_SRC_U8}
+
+
+def pack_volume(src: torch.Tensor, dims, order: int, dtype=torch.float32,
+                clamp_negative: bool = False) -> torch.Tensor:
+    """``drr_volume_pack``: a device tensor holding the volume in ``order``
+    (``DRR_ORDER_XFASTEST`` flat, or ``DRR_ORDER_ZFASTEST`` = a C-ordered
+    (nx, ny, nz) array) -> the walk's x-fastest flat layout in ``dtype``, cast
+    (and clamped) in the same pass."""
+    import ctypes
+    _require_cuda(src, "volume")
+    if src.dtype not in _SRC_CODES:
+        src = src.to(torch.float64)
+    src = src.contiguous()
+    n = [int(x) for x in dims]
+    out = torch.empty(n[0] * n[1] * n[2], dtype=dtype, device=src.device)
+    d = (ctypes.c_int64 * 3)(*n)
+    _lib.check(_lib.load().drr_volume_pack(
+        src.data_ptr(), _SRC_CODES[src.dtype], order, d, 1 if clamp_negative else 0,
+        out.data_ptr(), _lib.DRR_VOL_F32 if dtype == torch.float32 else _lib.DRR_VOL_F64,
+        _stream_ptr(src.device)))
+    return out
+
+
 class DeviceVolume:
     """A CT volume resident in HBM: float32, x-fastest, plus its grid."""
 
@@ -63,29 +88,49 @@ class DeviceVolume:
         self.spacing = spacing
         self.origin = origin
         self.dtype = dtype
-        # [i, j, k] -> x-fastest flat: memory order (k, j, i).
-        self.flat = t.to(device=device, dtype=dtype).permute(2, 1, 0).contiguous().reshape(-1)
+        # [i, j, k] (C order: z fastest) -> the x-fastest flat layout, on the device
+        self.flat = pack_volume(t.to(device), self.dims, _lib.DRR_ORDER_ZFASTEST, dtype)
         self.vol_dtype = _lib.DRR_VOL_F32 if dtype == torch.float32 else _lib.DRR_VOL_F64
         self.grid = _lib.make_grid(self.dims, self.spacing, self.origin)
 
     @classmethod
     def from_flat(cls, flat, dims, spacing, origin=(0.0, 0.0, 0.0), device=None,
-                  dtype=torch.float32):
-        """From an x-fastest flat array (the reference's ``flat_data()``)."""
-        arr = np.asarray(flat).reshape(tuple(int(n) for n in dims)[::-1])  # (nz, ny, nx)
-        return cls(np.transpose(arr, (2, 1, 0)), spacing, origin, device, dtype)
+                  dtype=torch.float32, clamp_negative: bool = False):
+        """From an x-fastest flat array (the reference's ``flat_data()``, .dvol /
+        raw payloads): uploaded as-is, cast (and clamped) by drr_volume_pack."""
+        dims = tuple(int(n) for n in dims)
+        if isinstance(flat, torch.Tensor):
+            src = flat.detach().reshape(-1)
+        else:
+            arr = np.asarray(flat).reshape(-1)
+            src = torch.as_tensor(arr if arr.flags.writeable else arr.copy())
+        if src.numel() != int(np.prod(dims)):
+            raise InvalidArgumentError(
+                f"data has {src.numel()} values, expected {int(np.prod(dims))} for dims {dims}")
+        self = cls.empty(dims, spacing, origin, device=device, dtype=dtype, allocate=False)
+        self.flat = pack_volume(src.to(self.flat.device), dims, _lib.DRR_ORDER_XFASTEST, dtype,
+                                clamp_negative)
+        return self
 
     @classmethod
-    def empty(cls, dims, spacing, origin=(0.0, 0.0, 0.0), device=None, dtype=torch.float32):
+    def empty(cls, dims, spacing, origin=(0.0, 0.0, 0.0), device=None, dtype=torch.float32,
+              allocate: bool = True):
         """Uninitialised device volume of the given dims (filled by the caller,
         e.g. a broadcast of another rank's ``flat``)."""
         self = cls.__new__(cls)
         self.dims = tuple(int(n) for n in dims)
         self.spacing = tuple(float(s) for s in np.broadcast_to(np.asarray(spacing, np.float64), (3,)))
         self.origin = tuple(float(s) for s in np.broadcast_to(np.asarray(origin, np.float64), (3,)))
+        if len(self.dims) != 3 or any(n < 1 for n in self.dims):
+            raise InvalidArgumentError(f"dims must be three integers >= 1, got {self.dims}")
+        if any(not (s > 0 and np.isfinite(s)) for s in self.spacing):
+            raise InvalidArgumentError(f"spacing must be three positive reals, got {self.spacing}")
+        if any(not np.isfinite(b) for b in self.origin):
+            raise InvalidArgumentError(f"plane_origin must be finite, got {self.origin}")
         self.dtype = dtype
         device = torch.device(device) if device is not None else torch.device("cuda")
-        self.flat = torch.empty(int(np.prod(self.dims)), dtype=dtype, device=device)
+        self.flat = (torch.empty(int(np.prod(self.dims)), dtype=dtype, device=device)
+                     if allocate else torch.empty(0, dtype=dtype, device=device))
         self.vol_dtype = _lib.DRR_VOL_F32 if dtype == torch.float32 else _lib.DRR_VOL_F64
         self.grid = _lib.make_grid(self.dims, self.spacing, self.origin)
         return self

@@ -4,10 +4,10 @@ Restates the reference's ``load_volume`` / ``import_raw``
 (``pkg/src/drrtrace/volume.py:149-222``): the ``.dvol`` format is one JSON
 header line (dims, spacing, origin, dtype "f64") followed by little-endian
 float64 densities in x-fastest order -- which IS the device layout, so the
-payload is uploaded as-is and narrowed to fp32 on the GPU (no host-side
-transpose or cast).  ``import_raw`` reads headerless f32 / i16 / u8 voxels,
-casts without Hounsfield rescaling and optionally clamps negatives, also on
-the device.  Errors mirror the reference (HeaderParseError with the byte
+payload is uploaded as-is and narrowed to fp32 on the GPU by
+``drr_volume_pack`` (no host-side transpose or cast).  ``import_raw`` reads
+headerless f32 / i16 / u8 voxels, uploads them in their own element type and
+lets the same kernel cast (no Hounsfield rescaling) and clamp negatives.  Errors mirror the reference (HeaderParseError with the byte
 offset, CorruptFileError on size mismatches, InvalidArgumentError).
 """
 
@@ -22,26 +22,6 @@ from .errors import CorruptFileError, HeaderParseError, InvalidArgumentError
 from .renderer import DeviceVolume
 
 _RAW_DTYPES = {"f32": "<f4", "i16": "<i2", "u8": "u1"}
-
-
-def _device_volume(flat_dev: torch.Tensor, dims, spacing, origin, dtype) -> DeviceVolume:
-    """Wrap an x-fastest flat device tensor as a DeviceVolume (no reorder)."""
-    vol = DeviceVolume.__new__(DeviceVolume)
-    from . import _lib
-    spacing = tuple(float(s) for s in np.broadcast_to(np.asarray(spacing, dtype=np.float64), (3,)))
-    origin = tuple(float(s) for s in np.broadcast_to(np.asarray(origin, dtype=np.float64), (3,)))
-    if any(not (s > 0 and np.isfinite(s)) for s in spacing):
-        raise InvalidArgumentError(f"spacing must be three positive reals, got {spacing}")
-    if any(not np.isfinite(b) for b in origin):
-        raise InvalidArgumentError(f"plane_origin must be finite, got {origin}")
-    vol.dims = tuple(int(n) for n in dims)
-    vol.spacing = spacing
-    vol.origin = origin
-    vol.dtype = dtype
-    vol.flat = flat_dev.to(dtype).contiguous()
-    vol.vol_dtype = _lib.DRR_VOL_F32 if dtype == torch.float32 else _lib.DRR_VOL_F64
-    vol.grid = _lib.make_grid(vol.dims, vol.spacing, vol.origin)
-    return vol
 
 
 def load_dvol(path, device=None, dtype=torch.float32) -> DeviceVolume:
@@ -71,7 +51,8 @@ def load_dvol(path, device=None, dtype=torch.float32) -> DeviceVolume:
         raise CorruptFileError(f"{path}: payload has {len(payload)} bytes, header declares {expected}")
     dev = torch.device(device) if device is not None else torch.device("cuda")
     flat = torch.frombuffer(bytearray(payload), dtype=torch.float64).to(dev)
-    return _device_volume(flat, dims, header["spacing"], header["origin"], dtype)
+    return DeviceVolume.from_flat(flat, dims, header["spacing"], header["origin"], device=dev,
+                                  dtype=dtype)
 
 
 def save_dvol(vol: DeviceVolume, path) -> None:
@@ -104,7 +85,6 @@ def import_raw(path, dims, spacing, plane_origin=(0.0, 0.0, 0.0), element_type: 
     if not host.dtype.isnative:
         host = host.astype(host.dtype.newbyteorder("="))
     dev = torch.device(device) if device is not None else torch.device("cuda")
-    flat = torch.from_numpy(host.copy()).to(dev).to(torch.float64)
-    if clamp_negative:
-        flat = torch.clamp_min(flat, 0.0)
-    return _device_volume(flat, dims, spacing, plane_origin, dtype)
+    raw = torch.from_numpy(host.copy()).to(dev)  # the file's own element type
+    return DeviceVolume.from_flat(raw, dims, spacing, plane_origin, device=dev, dtype=dtype,
+                                  clamp_negative=clamp_negative)

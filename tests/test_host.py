@@ -109,15 +109,16 @@ def test_module_validation_errors():
         DeviceVolume(np.zeros((4, 4, 4)), (1.0, 0.0, 1.0), device="cpu")
 
 
-def test_device_volume_layout_is_x_fastest():
-    """[i, j, k] = (x, y, z) -> flat i + nx (j + ny k) (volume.py:77-79)."""
-    from paper_2208_12737_b200 import DeviceVolume
+def test_device_volume_needs_cuda():
+    """No CPU fallback: the layout pass is drr_volume_pack on the device (its
+    x-fastest parity is tests/test_gpu_volume_pack.py), so a CPU device fails
+    loudly instead of silently packing on the host."""
+    from paper_2208_12737_b200 import DeviceVolume, InvalidArgumentError
     data = np.arange(2 * 3 * 4, dtype=np.float64).reshape(2, 3, 4)
-    v = DeviceVolume(data, 1.0, device="cpu", dtype=torch.float64)
-    np.testing.assert_array_equal(v.flat.numpy(), data.ravel(order="F"))
-    v2 = DeviceVolume.from_flat(data.ravel(order="F"), (2, 3, 4), 1.0, device="cpu",
-                                dtype=torch.float64)
-    np.testing.assert_array_equal(v2.flat.numpy(), v.flat.numpy())
+    with pytest.raises(InvalidArgumentError):
+        DeviceVolume(data, 1.0, device="cpu", dtype=torch.float64)
+    with pytest.raises(InvalidArgumentError):
+        DeviceVolume.from_flat(data.ravel(order="F"), (2, 3, 4), 1.0, device="cpu")
 
 
 def test_gimbal_guard_host():

@@ -1,5 +1,7 @@
 """Volume ingest (volume_io.py) vs the reference's .dvol / raw formats
-(volume.py:149-222): round trips and the same error classes.  CPU tensors."""
+(volume.py:149-222): round trips through the device layout pass
+(drr_volume_pack, -m gpu) and the same error classes (CPU: they are raised
+before anything reaches the device)."""
 
 import json
 
@@ -17,22 +19,24 @@ def _write_dvol(path, data, spacing=(1.0, 2.0, 0.5), origin=(-1.0, 0.0, 3.0)):
         fh.write(np.asarray(data, dtype="<f8").ravel(order="F").tobytes())
 
 
-def test_dvol_round_trip(tmp_path):
+@pytest.mark.gpu
+def test_dvol_round_trip(tmp_path, cuda_device):
     from paper_2208_12737_b200.volume_io import load_dvol, save_dvol
     data = np.random.default_rng(0).random((4, 5, 6))
     p = tmp_path / "v.dvol"
     _write_dvol(p, data)
-    vol = load_dvol(p, device="cpu", dtype=torch.float64)
+    vol = load_dvol(p, device=cuda_device, dtype=torch.float64)
     assert vol.dims == (4, 5, 6) and vol.spacing == (1.0, 2.0, 0.5) and vol.origin == (-1.0, 0.0, 3.0)
-    np.testing.assert_array_equal(vol.flat.numpy(), data.ravel(order="F"))
-    vol32 = load_dvol(p, device="cpu")
-    np.testing.assert_array_equal(vol32.flat.numpy(), data.ravel(order="F").astype(np.float32))
+    np.testing.assert_array_equal(vol.flat.cpu().numpy(), data.ravel(order="F"))
+    vol32 = load_dvol(p, device=cuda_device)
+    np.testing.assert_array_equal(vol32.flat.cpu().numpy(), data.ravel(order="F").astype(np.float32))
     q = tmp_path / "w.dvol"
     save_dvol(vol, q)
     assert q.read_bytes() == p.read_bytes()
 
 
-def test_dvol_matches_reference_writer(tmp_path):
+@pytest.mark.gpu
+def test_dvol_matches_reference_writer(tmp_path, cuda_device):
     dt = O.reference_module()
     if dt is None:
         pytest.skip("reference not built here")
@@ -40,8 +44,8 @@ def test_dvol_matches_reference_writer(tmp_path):
     ref = dt.make_phantom("sphere", (6, 7, 8), (1.0, 0.5, 2.0))
     p = tmp_path / "r.dvol"
     dt.save_volume(ref, p)
-    vol = load_dvol(p, device="cpu", dtype=torch.float64)
-    np.testing.assert_array_equal(vol.flat.numpy(), ref.flat_data())
+    vol = load_dvol(p, device=cuda_device, dtype=torch.float64)
+    np.testing.assert_array_equal(vol.flat.cpu().numpy(), ref.flat_data())
     assert vol.dims == ref.dims and vol.spacing == ref.spacing and vol.origin == ref.plane_origin
 
 
@@ -64,16 +68,24 @@ def test_dvol_errors(tmp_path):
         load_dvol(p, device="cpu")
 
 
-def test_import_raw(tmp_path):
+@pytest.mark.gpu
+def test_import_raw(tmp_path, cuda_device):
+    from paper_2208_12737_b200.volume_io import import_raw
+    data = np.arange(-12, 12, dtype=np.int16).reshape((2, 3, 4), order="F")
+    p = tmp_path / "v.raw"
+    p.write_bytes(data.ravel(order="F").astype("<i2").tobytes())
+    vol = import_raw(p, (2, 3, 4), 1.5, element_type="i16", device=cuda_device, dtype=torch.float64)
+    np.testing.assert_array_equal(vol.flat.cpu().numpy(), data.ravel(order="F").astype(np.float64))
+    vol = import_raw(p, (2, 3, 4), 1.5, element_type="i16", clamp_negative=True, device=cuda_device)
+    assert float(vol.flat.min()) == 0.0 and float(vol.flat.max()) == 11.0
+
+
+def test_import_raw_errors(tmp_path):
     from paper_2208_12737_b200.errors import CorruptFileError, InvalidArgumentError
     from paper_2208_12737_b200.volume_io import import_raw
     data = np.arange(-12, 12, dtype=np.int16).reshape((2, 3, 4), order="F")
     p = tmp_path / "v.raw"
     p.write_bytes(data.ravel(order="F").astype("<i2").tobytes())
-    vol = import_raw(p, (2, 3, 4), 1.5, element_type="i16", device="cpu", dtype=torch.float64)
-    np.testing.assert_array_equal(vol.flat.numpy(), data.ravel(order="F").astype(np.float64))
-    vol = import_raw(p, (2, 3, 4), 1.5, element_type="i16", clamp_negative=True, device="cpu")
-    assert float(vol.flat.min()) == 0.0 and float(vol.flat.max()) == 11.0
     with pytest.raises(CorruptFileError):
         import_raw(p, (2, 3, 5), 1.0, element_type="i16", device="cpu")
     with pytest.raises(InvalidArgumentError):
