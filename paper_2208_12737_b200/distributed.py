@@ -30,6 +30,7 @@ Under a world of one process every call is the single-GPU path.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -120,7 +121,8 @@ def rank_sync(device, group=None) -> None:
         flag = _sync_flag(device)
         dist.all_reduce(flag, group=group)
     else:
-        torch.cuda.synchronize(device)
+        if torch.device(device).type == "cuda":
+            torch.cuda.synchronize(device)
         dist.barrier(group=group)
 
 
@@ -141,10 +143,17 @@ class PeerRows:
     ``dst`` allocates it and exports it (``drr_peer_export``); the handle goes
     to the other ranks over the process group once, and each opens it on its
     own device (``drr_peer_open``: a pointer valid for its kernels, peer access
-    over NVLink).  ``ptr(row)`` is that rank's address of a row.  Collective:
-    every rank of ``group`` constructs it with the same arguments."""
+    over NVLink).  ``ptr(row)`` is that rank's address of a global row.
+    Collective: every rank of ``group`` constructs it with the same arguments.
 
-    def __init__(self, n_rows: int, row_shape, dtype, device, group=None, dst: int = 0):
+    If any rank cannot open the handle (no peer access between its GPU and
+    ``dst``'s, e.g. a launcher that hides the other GPUs from each process),
+    every rank falls back to a local buffer for its own rows ``[lo, hi)`` and
+    :meth:`collect` gathers them into ``dst``'s buffer with one NCCL
+    all-gather (``mode == "collective"``; the peer path is ``"peer"``)."""
+
+    def __init__(self, n_rows: int, row_shape, dtype, device, group=None, dst: int = 0,
+                 shard=None):
         self.world, self.rank = _world(group)
         self.group, self.dst = group, dst
         self.n_rows = int(n_rows)
@@ -153,8 +162,13 @@ class PeerRows:
         self.device = torch.device(device)
         self.row_bytes = int(np.prod(self.row_shape, dtype=np.int64)) * torch.empty(
             (), dtype=dtype).element_size()
+        self.lo, self.hi = shard if shard is not None else shard_range(self.n_rows, self.rank,
+                                                                       self.world)
         self.buf = None
+        self.local = None
         self._opened = None
+        self.mode = "peer"
+        self.row0 = 0  # global row at self.base
         lib = _lib.load()
         if self.rank == dst:
             self.buf = torch.empty((max(self.n_rows, 1),) + self.row_shape, dtype=dtype,
@@ -162,21 +176,55 @@ class PeerRows:
             self.base = self.buf.data_ptr()
         if self.world == 1:
             return
-        msg = [None]
-        if self.rank == dst:
-            h = _lib.DrrPeerHandle()
-            _lib.check(lib.drr_peer_export(self.buf.data_ptr(), ctypes.byref(h)))
-            msg = [bytes(h)]
-        dist.broadcast_object_list(msg, src=_global_rank(group, dst), group=group)
-        if self.rank != dst:
-            h = _lib.DrrPeerHandle.from_buffer_copy(msg[0])
-            p = ctypes.c_void_p()
-            _lib.check(lib.drr_peer_open(ctypes.byref(h), ctypes.byref(p)))
-            self.base = int(p.value)
-            self._opened = (self.base, int(h.offset))
+        forced = os.environ.get("DRR_PEER_MODE") == "collective"  # test knob
+        ok = 0 if forced else 1
+        if not forced:
+            msg = [None]
+            if self.rank == dst:
+                h = _lib.DrrPeerHandle()
+                _lib.check(lib.drr_peer_export(self.buf.data_ptr(), ctypes.byref(h)))
+                msg = [bytes(h)]
+            dist.broadcast_object_list(msg, src=_global_rank(group, dst), group=group)
+            if self.rank != dst:
+                h = _lib.DrrPeerHandle.from_buffer_copy(msg[0])
+                p = ctypes.c_void_p()
+                if lib.drr_peer_open(ctypes.byref(h), ctypes.byref(p)) == _lib.DRR_OK:
+                    self.base = int(p.value)
+                    self._opened = (self.base, int(h.offset))
+                else:
+                    ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32,
+                                device=self.device if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            ok = int(flag.item())
+        if ok == 0:
+            self.close()
+            self.mode = "collective"
+            if self.rank != dst:
+                self.local = torch.empty((max(self.hi - self.lo, 1),) + self.row_shape,
+                                         dtype=dtype, device=self.device)
+                self.base = self.local.data_ptr()
+                self.row0 = self.lo
+
+    def shard_view(self) -> torch.Tensor:
+        """This rank's rows [lo, hi) as a tensor it may write (collective mode,
+        or the collecting rank)."""
+        if self.rank == self.dst:
+            return self.buf[self.lo:self.hi]
+        if self.local is None:
+            raise RuntimeError("peer mode: this rank's rows live in the collecting rank's HBM")
+        return self.local[:self.hi - self.lo]
 
     def ptr(self, row: int = 0) -> int:
-        return self.base + int(row) * self.row_bytes
+        return self.base + (int(row) - self.row0) * self.row_bytes
+
+    def collect(self) -> None:
+        """Collective mode only: bring every rank's rows into ``dst``'s buffer."""
+        if self.mode != "collective":
+            return
+        allrows = gather_rows(self.shard_view(), self.n_rows, self.group)
+        if self.rank == self.dst:
+            self.buf[:self.n_rows].copy_(allrows)
 
     def rows(self, n: int | None = None) -> torch.Tensor | None:
         """The buffer's first n rows on ``dst`` (None on the other ranks)."""
@@ -265,7 +313,9 @@ class ShardedDRR:
             e = torch.as_tensor(np.asarray(eta, dtype=np.float64)[lo:hi], device=self.device)
         return n, lo, e.contiguous()
 
-    def _finish(self, out, copy):
+    def _finish(self, out, copy, peers=()):
+        for p in peers:
+            p.collect()
         rank_sync(self.device, self.group)
         if self.rank != self.dst:
             return None
@@ -299,7 +349,7 @@ class ShardedDRR:
                 _lib.check(lib.drr_forward(self.volume.flat.data_ptr(), self.volume.vol_dtype,
                                            self.volume.grid, fr[c0:].data_ptr(), c1 - c0, det.c,
                                            out.ptr(lo + c0), 0, st))
-        r = self._finish((out.rows(),), copy)
+        r = self._finish((out.rows(),), copy, (out,))
         return None if r is None else r[0]
 
     def loss_and_gradient(self, eta, fixed, loss_kind: str = "neg_zncc", copy: bool = True,
@@ -334,7 +384,7 @@ class ShardedDRR:
                               fixed_t, stride, LOSS_KINDS[loss_kind], buf, st,
                               value_ptr=vals.ptr(lo), grad_eta_ptr=grads.ptr(lo),
                               grad_frames=False)
-        return self._finish((vals.rows(), grads.rows()), copy)
+        return self._finish((vals.rows(), grads.rows()), copy, (vals, grads))
 
     def register_batch(self, fixed_images, poses0, config=None, use_graph: bool = True):
         """The population study (``cli.py:133-145``): ``len(poses0)`` independent
@@ -378,7 +428,6 @@ class ShardedDRR:
 def init_from_env(backend: str | None = None):
     """torchrun convenience: one process per GPU (LOCAL_RANK), NCCL over
     NVLink; returns (rank, world, device)."""
-    import os
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

@@ -5,7 +5,8 @@ from rank 0, each rank walks its block of the global pose batch, and its
 kernels store images / loss values / pose gradients straight into rank 0's
 buffers through the peer-memory ABI (drr_peer_export / drr_peer_open: CUDA
 IPC, the same mechanism that carries the stores over NVLink on a multi-GPU
-node).  Rank 0's gathered results must equal the single-process batch bit for
+node) -- or, in the "collective" fallback (peer access unavailable), into
+local rows gathered by one collective.  Rank 0's gathered results must equal the single-process batch bit for
 bit: the partition has no exchange step, so sharding may not
 change any result.  Registration traces of the population study are gathered
 in global order and equal single-process traces.
@@ -40,10 +41,12 @@ def _inputs():
     return vol, poses
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, peer_mode="peer"):
     import faulthandler
     import traceback
     faulthandler.enable(open(os.path.join(out_dir, f"fault{rank}.txt"), "w"))
+    if peer_mode == "collective":
+        os.environ["DRR_PEER_MODE"] = "collective"
     try:
         _work(rank, world, port, out_dir)
     except BaseException:
@@ -74,11 +77,13 @@ def _work(rank, world, port, out_dir):
     vol, poses = _inputs()
     sd = ShardedDRR(vol if rank == 0 else None, SP, 150.0, 33, 3.0, width=29,
                     device="cuda:0", ray_split=1)
+    want = "collective" if os.environ.get("DRR_PEER_MODE") == "collective" else "peer"
     fixed = sd.render(np.asarray([TRUTH]))
     fixed_all = [fixed.cpu() if rank == 0 else None]
     dist.broadcast_object_list(fixed_all, src=0)
     fixed = fixed_all[0][0].numpy()
     img = sd.render(poses)
+    assert all(p.mode == want for p in sd._peer.values()), [p.mode for p in sd._peer.values()]
     img2 = sd.render(poses[::-1].copy())           # buffers reused across calls
     lg = sd.loss_and_gradient(poses, fixed)
     cfg = OptimizerConfig(max_iters=12)
@@ -97,14 +102,15 @@ def _work(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_two_ranks_match_single_process(cuda_device, tmp_path):
+@pytest.mark.parametrize("peer_mode", ["peer", "collective"])
+def test_two_ranks_match_single_process(cuda_device, tmp_path, peer_mode):
     import torch
     import torch.multiprocessing as mp
     from paper_2208_12737_b200 import DeviceVolume, Detector, pose_frames, render_frames
     from paper_2208_12737_b200.registration import (OptimizerConfig, loss_and_gradient,
                                                     register_batch)
     try:
-        mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+        mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), peer_mode), nprocs=2, join=True)
     except Exception as exc:
         raise AssertionError(f"{exc}\n{_errors(str(tmp_path))}") from None
     got = dict(np.load(tmp_path / "sharded.npz"))
