@@ -42,6 +42,8 @@
  *                               walk per ray, no stored Jacobian
  *   drr_register_update      <- one iteration of registration.py:89-125
  *                               register() (momentum GD + convergence state)
+ *   drr_volume_bounds        <- no counterpart: the occupied box that lets
+ *                               the walks skip exactly-zero margins
  *   drr_volume_pack          <- volume.py:77-79 flat_data() (the x-fastest
  *                               layout) + volume.py:196-222 import_raw's cast
  *                               and clamp, as one device pass
@@ -74,11 +76,18 @@ extern "C" {
 #define DRR_VOL_F64 1 /* drop-in for the reference's float64 flat volume  */
 
 /* Axis-aligned voxel grid: dims[a] voxels of spacing[a] mm, planes at
- * origin[a] + k*spacing[a], k = 0..dims[a]   (volume.py:24-60). */
+ * origin[a] + k*spacing[a], k = 0..dims[a]   (volume.py:24-60).
+ * occ_lo / occ_hi (optional): the voxel-index box [occ_lo, occ_hi) outside of
+ * which every voxel is exactly zero (drr_volume_bounds).  The walks then run
+ * over that box only -- segments outside it add nothing to any sum, so every
+ * image and gradient is bit-identical to the full walk.  All-zero occ_hi
+ * means the whole volume. */
 typedef struct drr_grid {
   int64_t dims[3];
   double spacing[3];
   double origin[3];
+  int64_t occ_lo[3];
+  int64_t occ_hi[3];
 } drr_grid;
 
 /* Detector: H x W pixels, pitch_x along W, pitch_y along H (geometry.py:71-97,
@@ -154,6 +163,13 @@ int drr_backward_jac(const double *d_jac, int32_t n_poses,
                      const drr_detector *det, const void *d_grad_img,
                      int grad_dtype, double *d_grad_frames, void *d_workspace,
                      size_t workspace_bytes, void *stream);
+
+/* The occupied box of a device volume in the walk's layout: per axis the
+ * voxel-index range [lo, hi) holding every voxel that is not exactly zero
+ * (NaN counts as nonzero, -0.0 as zero).  An all-zero volume
+ * gives lo = hi = 0.  d_bounds: 6 int32 device ints (lo[3], hi[3]). */
+int drr_volume_bounds(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                      int32_t *d_bounds, void *stream);
 
 /* One-time ingest of a device volume into the walk's layout: x-fastest
  * (flat = i + nx (j + ny k), volume.py:77-79), dst_dtype DRR_VOL_F32 / F64.

@@ -38,6 +38,7 @@ EXPORTS = (
     "drr_backward_jac",
     "drr_count_steps",
     "drr_volume_pack",
+    "drr_volume_bounds",
     "drr_signature",
     "drr_pose_frames",
     "drr_pose_grad",
@@ -54,7 +55,9 @@ EXPORTS = (
 class DrrGrid(ctypes.Structure):
     _fields_ = [("dims", ctypes.c_int64 * 3),
                 ("spacing", ctypes.c_double * 3),
-                ("origin", ctypes.c_double * 3)]
+                ("origin", ctypes.c_double * 3),
+                ("occ_lo", ctypes.c_int64 * 3),
+                ("occ_hi", ctypes.c_int64 * 3)]
 
 
 class DrrRegConfig(ctypes.Structure):
@@ -99,6 +102,7 @@ _SIGNATURES = {
     "drr_backward_jac": ([_vp, _i32, _DP, _vp, _int, _vp, _vp, _sz, _vp], _int),
     "drr_count_steps": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
     "drr_volume_pack": ([_vp, _int, _int, ctypes.POINTER(_i64), _int, _vp, _int, _vp], _int),
+    "drr_volume_bounds": ([_vp, _int, _GP, _vp, _vp], _int),
     "drr_signature": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
     "drr_pose_frames": ([_vp, _i32, ctypes.POINTER(ctypes.c_double), _vp, _vp], _int),
     "drr_pose_grad": ([_vp, _vp, _i32, _vp, _vp], _int),
@@ -154,12 +158,16 @@ def check(rc: int) -> None:
     raise KernelError(f"drr status {rc}: {msg}")
 
 
-def make_grid(dims, spacing, origin) -> DrrGrid:
+def make_grid(dims, spacing, origin, occupied=None) -> DrrGrid:
+    """The C grid; ``occupied`` = ((lo0, lo1, lo2), (hi0, hi1, hi2)), the voxel
+    box outside of which the volume is exactly zero (None: the whole volume)."""
     g = DrrGrid()
     for a in range(3):
         g.dims[a] = int(dims[a])
         g.spacing[a] = float(spacing[a])
         g.origin[a] = float(origin[a])
+        g.occ_lo[a] = int(occupied[0][a]) if occupied is not None else 0
+        g.occ_hi[a] = int(occupied[1][a]) if occupied is not None else 0
     return g
 
 

@@ -63,9 +63,11 @@ _VOL_CACHE_MAX = 2
 
 
 def _device_volume(flat_data, dims, dev):
+    """(device volume, its occupied box) -- cached for read-only volumes."""
     arr = np.asarray(flat_data).reshape(-1)
     if arr.flags.writeable:
-        return _upload(arr, dev)
+        d = _upload(arr, dev)
+        return d, _bounds(d, dims)
     key = (arr.__array_interface__["data"][0], arr.nbytes, arr.dtype.str,
            tuple(int(n) for n in dims), str(dev))
     hit = _VOL_CACHE.get(key)
@@ -74,15 +76,21 @@ def _device_volume(flat_data, dims, dev):
     while len(_VOL_CACHE) >= _VOL_CACHE_MAX:
         _VOL_CACHE.pop(next(iter(_VOL_CACHE)))
     d = _upload(arr, dev)
-    _VOL_CACHE[key] = (arr, d)
-    return d
+    _VOL_CACHE[key] = (arr, (d, _bounds(d, dims)))
+    return _VOL_CACHE[key][1]
+
+
+def _bounds(vol, dims):
+    from .renderer import volume_bounds
+    return volume_bounds(vol, _lib.make_grid(dims, (1.0, 1.0, 1.0), (0.0, 0.0, 0.0)),
+                         _lib.DRR_VOL_F64)
 
 
 def _prep(flat_data, dims, spacing, origin, source, pixels):
     dev = _device()
     pix = np.ascontiguousarray(np.atleast_2d(pixels), dtype=np.float64)
-    grid = _lib.make_grid(dims, spacing, origin)
-    vol = _device_volume(flat_data, dims, dev)
+    vol, occupied = _device_volume(flat_data, dims, dev)
+    grid = _lib.make_grid(dims, spacing, origin, occupied)
     src = _upload(np.asarray(source).reshape(3), dev)
     return dev, grid, vol, src, _upload(pix, dev), pix.shape[0]
 

@@ -540,6 +540,63 @@ __global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
   }
 }
 
+// ------------------------------------------------------------ occupied box
+// Per axis the min / max voxel index of any voxel that is not exactly zero
+// (NaN counts as occupied), by integer atomics: order-free, so deterministic.
+// out: lo[3] (init n), hi[3] (init -1, stored as max index; the host adds 1).
+template <typename VT>
+__global__ void __launch_bounds__(256)
+    k_volume_bounds(const VT* __restrict__ vol, const GridDev g, int* __restrict__ out) {
+  int lo[3] = {g.n[0], g.n[1], g.n[2]}, hi[3] = {-1, -1, -1};
+  const int64_t n = g.total;
+  for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const VT v = vol[f];
+    if (!(v == VT(0))) {
+      const int i = static_cast<int>(f % g.n[0]);
+      const int j = static_cast<int>((f / g.n[0]) % g.n[1]);
+      const int k = static_cast<int>(f / (static_cast<int64_t>(g.n[0]) * g.n[1]));
+      lo[0] = min(lo[0], i); hi[0] = max(hi[0], i);
+      lo[1] = min(lo[1], j); hi[1] = max(hi[1], j);
+      lo[2] = min(lo[2], k); hi[2] = max(hi[2], k);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], off));
+      hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], off));
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(out + a, lo[a]);
+      atomicMax(out + 3 + a, hi[a]);
+    }
+  }
+}
+
+__global__ void k_bounds_init(const GridDev g, int* out) {
+  if (threadIdx.x < 3) {
+    out[threadIdx.x] = g.n[threadIdx.x];
+    out[3 + threadIdx.x] = -1;
+  }
+}
+
+__global__ void k_bounds_finish(int* out) {
+  // [lo, max] -> [lo, max + 1); an empty volume -> [0, 0) on every axis
+  if (threadIdx.x == 0) {
+    const bool empty = out[3] < 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      out[a] = empty ? 0 : out[a];
+      out[3 + a] = empty ? 0 : out[3 + a] + 1;
+    }
+  }
+}
+
 // ------------------------------------------------------ discrete signature
 // Per pose, a 64-bit signature of every ray's traversal structure (SigVisitor:
 // labels, used set, voxels, exit selector; a missed ray hashes as a miss),
@@ -848,6 +905,20 @@ int make_grid(const drr_grid* in, drr::GridDev& g) {
   g.stride[1] = g.n[0];
   g.stride[2] = g.n[0] * g.n[1];
   g.total = static_cast<int>(total);
+  // the occupied box (drr_volume_bounds); all-zero occ_hi = the whole volume
+  const bool whole = in->occ_hi[0] == 0 && in->occ_hi[1] == 0 && in->occ_hi[2] == 0 &&
+                     in->occ_lo[0] == 0 && in->occ_lo[1] == 0 && in->occ_lo[2] == 0;
+  for (int a = 0; a < 3; ++a) {
+    const int64_t lo = whole ? 0 : in->occ_lo[a], hi = whole ? in->dims[a] : in->occ_hi[a];
+    if (lo < 0 || hi < lo || hi > in->dims[a])
+      return fail(DRR_ERR_INVALID_ARGUMENT, "occupied box [%lld, %lld) outside [0, %lld] on axis %d",
+                  (long long)lo, (long long)hi, (long long)in->dims[a], a);
+    // the plane table's rounding of P(k) = o + k*sp (whole volume: o and hi)
+    volatile double plo = static_cast<double>(lo) * in->spacing[a];
+    volatile double phi = static_cast<double>(hi) * in->spacing[a];
+    g.tlo[a] = in->origin[a] + plo;
+    g.thi[a] = in->origin[a] + phi;
+  }
   if (table_bytes(g, true) > 227 * 1024)
     return fail(DRR_ERR_INVALID_ARGUMENT, "plane table of %zu bytes exceeds shared memory",
                 table_bytes(g, true));
@@ -1324,6 +1395,28 @@ int drr_forward_loss_grad(const void* d_vol, int vol_dtype, const drr_grid* grid
   return check_launch("drr_forward_loss_grad/reduce");
 }
 
+int drr_volume_bounds(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                      int32_t* d_bounds, void* stream) {
+  drr::GridDev g;
+  const int rc = make_grid(grid, g);
+  if (rc) return rc;
+  if (d_vol == nullptr || d_bounds == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "drr_volume_bounds: NULL argument");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t blocks = (static_cast<int64_t>(g.total) + 255) / 256;
+  const unsigned grd = static_cast<unsigned>(blocks < 148 * 16 ? blocks : 148 * 16);
+  drr::k_bounds_init<<<1, 32, 0, st>>>(g, d_bounds);
+  if (vol_dtype == DRR_VOL_F32)
+    drr::k_volume_bounds<float><<<grd, 256, 0, st>>>(static_cast<const float*>(d_vol), g, d_bounds);
+  else if (vol_dtype == DRR_VOL_F64)
+    drr::k_volume_bounds<double><<<grd, 256, 0, st>>>(static_cast<const double*>(d_vol), g,
+                                                      d_bounds);
+  else
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
+  drr::k_bounds_finish<<<1, 32, 0, st>>>(d_bounds);
+  return check_launch("drr_volume_bounds");
+}
+
 int drr_signature(const void* d_vol, int vol_dtype, const drr_grid* grid,
                   const double* d_frames, int32_t n_poses, const drr_detector* det,
                   uint64_t* d_sig, void* stream) {
@@ -1331,6 +1424,10 @@ int drr_signature(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::DetDev d;
   int rc = make_grid(grid, g);
   if (rc) return rc;
+  for (int a = 0; a < 3; ++a) {  // the reference's structure includes the zero margins
+    g.tlo[a] = g.o[a];
+    g.thi[a] = g.hi[a];
+  }
   const size_t smem = table_bytes(g, false);
   rc = make_det(det, d);
   if (rc) return rc;

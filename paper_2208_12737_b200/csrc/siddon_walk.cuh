@@ -45,6 +45,11 @@ struct GridDev {
   double sp[3];
   double o[3];
   double hi[3];    // o + n*sp, as _native.pyx:34 computes it
+  // faces of the occupied box (every voxel outside it is exactly zero):
+  // P(lo) and P(hi) with P(k) = o + k*sp rounded as the plane table rounds it,
+  // so the trimmed entry / exit parameters are the walk's own crossing
+  // parameters of those planes; the whole volume gives tlo = o, thi = hi
+  double tlo[3], thi[3];
 };
 
 template <typename VT>
@@ -155,18 +160,26 @@ struct Ray {
 constexpr int kNoEndLab = 4;
 
 // Slab entry/exit, first-max/first-min labels over (x, y, z, clip):
-// _native.pyx:20-65.
+// _native.pyx:20-65.  The slab is the occupied box [tlo, thi] (GridDev): a
+// walk over it is the reference's walk over the whole volume with its
+// exactly-zero margins left out.  Every segment outside the box has value 0
+// and every crossing outside it coefficient 0 (value before = after = 0), so
+// acc, G and H receive the same nonzero terms in the same order; at the box
+// faces the entry / exit semantics (a virtual crossing at amin with the
+// first-max label, then every plane crossing with amin <= alpha <= amax,
+// ties to the lowest axis) put the same coefficient on the same crossing as
+// the full walk does.  Bit-identical results (tests/test_gpu_trim.py).
 __device__ __forceinline__ void entry_exit(const GridDev& g, Ray& r) {
   double cmin[3], cmax[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     if (r.d[a] == 0.0) {
-      const bool inside = (g.o[a] <= r.s[a]) && (r.s[a] <= g.hi[a]);
+      const bool inside = (g.tlo[a] <= r.s[a]) && (r.s[a] <= g.thi[a]);
       cmin[a] = inside ? -INFINITY : INFINITY;
       cmax[a] = inside ? INFINITY : -INFINITY;
     } else {
-      double a0 = (g.o[a] - r.s[a]) / r.d[a];
-      double a1 = (g.hi[a] - r.s[a]) / r.d[a];
+      double a0 = (g.tlo[a] - r.s[a]) / r.d[a];
+      double a1 = (g.thi[a] - r.s[a]) / r.d[a];
       if (a0 > a1) { const double t = a0; a0 = a1; a1 = t; }
       cmin[a] = a0;
       cmax[a] = a1;

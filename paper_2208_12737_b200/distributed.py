@@ -278,6 +278,9 @@ class ShardedDRR:
             dv = DeviceVolume.empty(dims, spacing, origin, device=self.device)
         if self.world > 1:
             dist.broadcast(dv.flat, src=_global_rank(group, src), group=group)
+        if self.rank != src:  # same data, so the same occupied box as rank src's
+            dv.trim = True
+            dv.refresh_bounds()
         self.volume = dv
         self.detector = Detector(height, width if width is not None else height, delx, dely,
                                  ray_split=ray_split)

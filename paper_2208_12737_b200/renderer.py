@@ -65,11 +65,26 @@ def pack_volume(src: torch.Tensor, dims, order: int, dtype=torch.float32,
     return out
 
 
+def volume_bounds(flat: torch.Tensor, grid, vol_dtype: int):
+    """``drr_volume_bounds``: ((lo0, lo1, lo2), (hi0, hi1, hi2)), the voxel box
+    outside of which the device volume is exactly zero (one sync)."""
+    out = torch.empty(6, dtype=torch.int32, device=flat.device)
+    _lib.check(_lib.load().drr_volume_bounds(flat.data_ptr(), vol_dtype, grid, out.data_ptr(),
+                                             _stream_ptr(flat.device)))
+    b = [int(x) for x in out.cpu().tolist()]
+    return tuple(b[:3]), tuple(b[3:])
+
+
 class DeviceVolume:
-    """A CT volume resident in HBM: float32, x-fastest, plus its grid."""
+    """A CT volume resident in HBM: float32, x-fastest, plus its grid.
+
+    ``trim`` (default): the grid carries the volume's occupied box
+    (:func:`volume_bounds`) and the walks skip its exactly-zero margins --
+    bit-identical results, fewer voxel-steps (``refresh_bounds`` after
+    writing into ``flat``)."""
 
     def __init__(self, data, spacing, origin=(0.0, 0.0, 0.0), device=None,
-                 dtype=torch.float32):
+                 dtype=torch.float32, trim: bool = True):
         spacing = tuple(float(s) for s in np.broadcast_to(np.asarray(spacing, dtype=np.float64), (3,)))
         origin = tuple(float(s) for s in np.broadcast_to(np.asarray(origin, dtype=np.float64), (3,)))
         if isinstance(data, torch.Tensor):
@@ -91,11 +106,26 @@ class DeviceVolume:
         # [i, j, k] (C order: z fastest) -> the x-fastest flat layout, on the device
         self.flat = pack_volume(t.to(device), self.dims, _lib.DRR_ORDER_ZFASTEST, dtype)
         self.vol_dtype = _lib.DRR_VOL_F32 if dtype == torch.float32 else _lib.DRR_VOL_F64
+        self.trim = trim
+        self.refresh_bounds()
+
+    def refresh_bounds(self):
+        """(Re)compute the grid: with ``trim``, the occupied box of ``flat``."""
         self.grid = _lib.make_grid(self.dims, self.spacing, self.origin)
+        self.occupied = None
+        if getattr(self, "trim", False) and self.flat.numel():
+            self.occupied = volume_bounds(self.flat, self.grid, self.vol_dtype)
+            self.grid = _lib.make_grid(self.dims, self.spacing, self.origin, self.occupied)
+        return self
+
+    @property
+    def full_grid(self):
+        """The grid without the occupied box (the reference's whole-volume walk)."""
+        return _lib.make_grid(self.dims, self.spacing, self.origin)
 
     @classmethod
     def from_flat(cls, flat, dims, spacing, origin=(0.0, 0.0, 0.0), device=None,
-                  dtype=torch.float32, clamp_negative: bool = False):
+                  dtype=torch.float32, clamp_negative: bool = False, trim: bool = True):
         """From an x-fastest flat array (the reference's ``flat_data()``, .dvol /
         raw payloads): uploaded as-is, cast (and clamped) by drr_volume_pack."""
         dims = tuple(int(n) for n in dims)
@@ -110,7 +140,8 @@ class DeviceVolume:
         self = cls.empty(dims, spacing, origin, device=device, dtype=dtype, allocate=False)
         self.flat = pack_volume(src.to(self.flat.device), dims, _lib.DRR_ORDER_XFASTEST, dtype,
                                 clamp_negative)
-        return self
+        self.trim = trim
+        return self.refresh_bounds()
 
     @classmethod
     def empty(cls, dims, spacing, origin=(0.0, 0.0, 0.0), device=None, dtype=torch.float32,
@@ -132,6 +163,8 @@ class DeviceVolume:
         self.flat = (torch.empty(int(np.prod(self.dims)), dtype=dtype, device=device)
                      if allocate else torch.empty(0, dtype=dtype, device=device))
         self.vol_dtype = _lib.DRR_VOL_F32 if dtype == torch.float32 else _lib.DRR_VOL_F64
+        self.trim = False  # contents unknown until filled: refresh_bounds(trim) then
+        self.occupied = None
         self.grid = _lib.make_grid(self.dims, self.spacing, self.origin)
         return self
 
@@ -260,14 +293,18 @@ def backward_from_jac(det: Detector, jac: torch.Tensor, grad_img: torch.Tensor) 
     return grad_frames
 
 
-def count_steps(vol: DeviceVolume, det: Detector, frames: torch.Tensor) -> torch.Tensor:
-    """Used voxel-steps per ray (B, H, W) int32 (python_ref.ray_structure's `use`)."""
+def count_steps(vol: DeviceVolume, det: Detector, frames: torch.Tensor,
+                full: bool = False) -> torch.Tensor:
+    """Used voxel-steps per ray (B, H, W) int32 (python_ref.ray_structure's `use`).
+    ``full``: of the reference's whole-volume walk (SURVEY 8(d)'s S), else of
+    the walk the kernels take (the occupied box only)."""
     frames = frames.detach().to(torch.float64).contiguous()
     B = frames.shape[0]
     steps = torch.empty((B, det.height, det.width), dtype=torch.int32, device=frames.device)
     lib = _lib.load()
+    grid = vol.full_grid if full else vol.grid
     for lo, hi in _pose_chunks(B):
-        _lib.check(lib.drr_count_steps(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
+        _lib.check(lib.drr_count_steps(vol.flat.data_ptr(), vol.vol_dtype, grid,
                                        frames[lo:hi].data_ptr(), hi - lo, det.c,
                                        steps[lo:hi].data_ptr(), _stream_ptr(frames.device)))
     return steps

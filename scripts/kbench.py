@@ -30,7 +30,7 @@ for B in [int(x) for x in (sys.argv[1:] or ["32", "1"])]:
     from paper_2208_12737_b200 import _lib
     from paper_2208_12737_b200.registration import _Buffers
     lib = _lib.load()
-    lb = _Buffers(drr.volume, drr.detector, B)
+    lb = _Buffers(drr.volume, drr.detector, B, mode="fused")
     et = torch.tensor(poses, device=dev)
     fixed = torch.rand((200, 200), device=dev)
 

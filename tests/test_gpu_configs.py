@@ -40,7 +40,7 @@ def test_c4_batched_generation(cuda_device):
         part = render_frames(vol, det, frames[lo:hi].contiguous())
         assert torch.equal(part, full[lo:hi]), (lo, hi)
     # used voxel-steps per DRR (38.7 M mean, 520-723 steps/ray)
-    steps = count_steps(vol, det, frames[:64].contiguous()).double()
+    steps = count_steps(vol, det, frames[:64].contiguous(), full=True).double()
     per_drr = float(steps.sum()) / 64
     assert 30e6 < per_drr < 45e6, per_drr
     # first and last pose against the oracle (fp32 densities fed as f64), one

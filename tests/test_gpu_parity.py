@@ -204,7 +204,7 @@ def test_c1_config(golden, cuda_device):
     from paper_2208_12737_b200 import render_frames
     img = render_frames(drr.volume, drr.detector, frame, out_dtype=torch.float64)
     np.testing.assert_array_equal(img[0].cpu().numpy(), golden["c1_image"])
-    steps = count_steps(drr.volume, drr.detector, frame)
+    steps = count_steps(drr.volume, drr.detector, frame, full=True)
     assert int(steps.sum()) == int(golden["c1_steps"])
     rot = torch.tensor(eta[1:4], device=cuda_device, requires_grad=True)
     tra = torch.tensor(eta[4:7], device=cuda_device, requires_grad=True)
