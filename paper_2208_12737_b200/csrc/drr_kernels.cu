@@ -966,17 +966,19 @@ int device_sms() {
 constexpr int kResidentCtasPerSm = 6;  // the walk kernels' launch bounds (DRR_*_MINB)
 
 // Threads per ray: explicit, or auto = the smallest K in {1, 2, 4, 8} with
-// B*H*W*K >= one wave of resident threads (SMs x 6 CTAs x 128; 148 SMs on a
-// B200).  A/B (scripts/kbench_split.py, one pose, fwd+jac+contraction /
-// forward ms for K = 1 / 2 / 4 / 8): C2 200^2 0.218 / 0.150 / 0.147 / 0.161
-// and 0.171 / 0.114 / 0.112 / 0.124 (K = 4 chosen; two waves would pick 8);
-// C1 100^2 forward 0.057 / 0.047 / 0.039 / 0.034 (K = 8).
+// B*H*W*K >= 0.6 waves of resident threads (SMs x 6 CTAs x 128; 148 SMs on
+// a B200).  A/B (scripts/kbench_split.py, one pose, fwd+jac+contraction /
+// forward ms for K = 1 / 2 / 4 / 8), with occupied-box trimming
+// (profiles/r02/rec1_kbench_split.json): C2 200^2 0.168 / 0.116 / 0.119 /
+// 0.130 and 0.129 / 0.082 / 0.085 / 0.097 (K = 2 chosen); C1 100^2 forward
+// 0.045 / 0.033 / 0.027 / 0.025 (K = 8).  (Untrimmed, r01: C2 0.218 / 0.150 /
+// 0.147 / 0.161 -- the shorter trimmed rays favour fewer, longer chunks.)
 int ray_split(const drr::DetDev& d, int n_poses) {
   if (d.split > 0) return d.split;
   const double rays = static_cast<double>(n_poses) * d.H * d.W;
   const double wave = static_cast<double>(device_sms()) * kResidentCtasPerSm * drr::kThreads;
   int k = 1;
-  while (k < 8 && rays * k < wave) k *= 2;
+  while (k < 8 && rays * k < 0.6 * wave) k *= 2;
   return k;
 }
 

@@ -27,10 +27,10 @@ def timed(fn, n=20):
 
 
 vol = DeviceVolume(synthetic.chest_phantom(), (0.703125, 0.703125, 2.5), device=dev)
-f = pose_frames(torch.tensor([[300.0, math.pi / 2, math.pi / 2, 0.0, 0.0, 0.0, 0.0]], device=dev),
+f = pose_frames(torch.tensor([[300.0, math.pi / 2, math.pi / 2, 0.0, 0.0, 0.0, 0.0]], dtype=torch.float64, device=dev),
                 vol.center).detach()
 v1 = DeviceVolume(synthetic.make_phantom("sphere", 128, 1.0), 1.0, device=dev)
-f1 = pose_frames(torch.tensor([[300.0, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0]], device=dev), v1.center).detach()
+f1 = pose_frames(torch.tensor([[300.0, 0.4, 1.3, 0.1, 0.0, 0.0, 0.0]], dtype=torch.float64, device=dev), v1.center).detach()
 g = torch.randn((1, 200, 200), device=dev)
 res = {}
 for K in (0, 1, 2, 4, 8):
