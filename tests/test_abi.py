@@ -74,10 +74,11 @@ def test_workspace_size_and_error():
     det = _lib.make_detector(200, 200, 3.6, 3.6, ray_split=1)
     # one thread per ray: 13 x 25 CTA tiles of 16 x 8 pixels, 12 doubles each, per pose
     assert lib.drr_backward_workspace_size(3, det) == 3 * 13 * 25 * 12 * 8
-    # auto split: one pose's 200^2 rays < one wave of resident threads (148 x 6 x 128)
-    # -> 4 threads per ray, 8 x 4 pixel tiles; three poses fill it -> one thread per ray
+    # auto split: one pose's 200^2 rays < 0.6 waves of resident threads (148 x 6 x 128;
+    # no device here: 148 SMs assumed) -> 2 threads per ray, 8 x 8 pixel tiles; three
+    # poses fill it -> one thread per ray
     auto = _lib.make_detector(200, 200, 3.6, 3.6)
-    assert lib.drr_backward_workspace_size(1, auto) == 1 * 25 * 50 * 12 * 8
+    assert lib.drr_backward_workspace_size(1, auto) == 1 * 25 * 25 * 12 * 8
     assert lib.drr_backward_workspace_size(3, auto) == 3 * 13 * 25 * 12 * 8
     # a large batch needs no split
     assert lib.drr_backward_workspace_size(64, auto) == 64 * 13 * 25 * 12 * 8

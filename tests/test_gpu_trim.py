@@ -1,10 +1,11 @@
-"""Occupied-box trimming (drr_volume_bounds; GridDev tlo / thi): the walks
-skip the exactly-zero margins of the volume, and every output must be
-bit-identical to the reference's whole-volume walk -- images, ray Jacobians,
-re-walk gradients, fused loss gradients, explicit-ray energies -- at C2 scale
-(the chest phantom's air margins), for a single split pose, and on volumes
-whose occupied box touches or misses the faces; the box itself against numpy
-(NaN counts as occupied, -0.0 as empty)."""
+"""Exact empty-space trimming: the occupied box (drr_volume_bounds; GridDev
+tlo / thi).  The walks skip the exactly-zero margins of the volume, and every
+output must be bit-identical to the reference's whole-volume walk -- images,
+ray Jacobians, re-walk gradients, fused loss gradients, explicit-ray
+energies -- at C2 scale (the chest phantom's air margins), on a ball in its
+bounding cube (C5's shape), on scattered blobs, for a single split pose, and
+on volumes whose occupied box touches or misses the faces; the box against
+numpy (NaN counts as occupied, -0.0 as empty)."""
 
 import math
 
@@ -45,6 +46,70 @@ def _pair(data, spacing, dev, dtype=torch.float32):
     a = DeviceVolume(data, spacing, device=dev, dtype=dtype)
     b = DeviceVolume(data, spacing, device=dev, dtype=dtype, trim=False)
     return a, b
+
+
+@pytest.mark.parametrize("kind", ["ball", "blobs"])
+def test_trim_bitwise_air_inside_box(cuda_device, kind):
+    """Shapes with air inside their bounding box (and rays that miss it)."""
+    from paper_2208_12737_b200 import (Detector, backward_frames, pose_frames, render_frames,
+                                       render_frames_jac, synthetic)
+    from paper_2208_12737_b200.registration import loss_and_gradient
+    n = 64
+    if kind == "ball":
+        data = synthetic.make_phantom("sphere", n, 1.0) + 3.0 * synthetic.make_phantom(
+            "off_center_cube", n, 1.0)
+    else:
+        rng = np.random.default_rng(9)
+        data = np.zeros((n, n, n))
+        for _ in range(7):
+            c = rng.integers(8, n - 8, 3)
+            data[c[0] - 4:c[0] + 4, c[1] - 3:c[1] + 5, c[2] - 5:c[2] + 2] = rng.random() + 0.5
+    tv, fv = _pair(data, 1.0, cuda_device)
+    det = Detector(96, 80, 1.4, ray_split=1)
+    eta = torch.tensor(synthetic.sample_poses((120.0, 0.7, 1.1, 0.2, 0, 0, 0),
+                                              synthetic.NARROW_HALF_WIDTHS, 6, seed=5),
+                       device=cuda_device)
+    fr = pose_frames(eta, tv.center).detach()
+    ib, jb = render_frames_jac(fv, det, fr)
+    ia, ja = render_frames_jac(tv, det, fr)
+    torch.testing.assert_close(ia, ib, rtol=0, atol=0)
+    torch.testing.assert_close(ja, jb, rtol=0, atol=0)
+    g = torch.randn((6, 96, 80), device=cuda_device)
+    torch.testing.assert_close(backward_frames(tv, det, fr, g), backward_frames(fv, det, fr, g),
+                               rtol=0, atol=0)
+    fixed = render_frames(fv, det, fr[:1])[0]
+    for mode in ("fused", "jac"):
+        va, ga = loss_and_gradient(tv, det, eta, fixed, mode=mode)
+        vb, gb = loss_and_gradient(fv, det, eta, fixed, mode=mode)
+        torch.testing.assert_close(va, vb, rtol=0, atol=0)
+        torch.testing.assert_close(ga, gb, rtol=0, atol=0)
+
+
+def test_trim_sources_inside_volume(cuda_device):
+    """A source inside the volume but outside the occupied box (clip entry):
+    images stay bitwise; the gradient sums may switch to the derived-axis form
+    of the walk when the trimmed start is a plane crossing instead of the clip
+    (1e-13)."""
+    from paper_2208_12737_b200 import backend_cuda, synthetic
+    data = synthetic.blob_phantom(48, 1.0)
+    flat = data.ravel(order="F").copy()
+    flat.flags.writeable = False
+    rng = np.random.default_rng(12)
+    src = np.array([3.0, 4.0, 2.5])  # inside the volume, in its air corner
+    pix = rng.uniform(-20, 70, (800, 3))
+    backend_cuda._VOL_CACHE.clear()
+    e_t, s_t, p_t = backend_cuda.ray_endpoint_grad(flat, (48,) * 3, (1.0,) * 3, (0.0,) * 3, src, pix)
+    w = flat.copy()  # writeable: uploaded per call; walked untrimmed here
+    orig = backend_cuda._bounds
+    backend_cuda._bounds = lambda vol, dims: ((0, 0, 0), tuple(int(n) for n in dims))
+    try:
+        e_f, s_f, p_f = backend_cuda.ray_endpoint_grad(w, (48,) * 3, (1.0,) * 3, (0.0,) * 3, src,
+                                                       pix)
+    finally:
+        backend_cuda._bounds = orig
+    np.testing.assert_array_equal(e_t, e_f)
+    for a, b in ((s_t, s_f), (p_t, p_f)):
+        np.testing.assert_allclose(a, b, rtol=1e-13, atol=1e-13 * np.abs(b).max())
 
 
 def test_c2_trimmed_walks_are_bitwise(cuda_device):
