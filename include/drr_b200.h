@@ -42,8 +42,8 @@
  *                               walk per ray, no stored Jacobian
  *   drr_register_update      <- one iteration of registration.py:89-125
  *                               register() (momentum GD + convergence state)
- *   drr_volume_bounds        <- no counterpart: the occupied box that lets
- *                               the walks skip exactly-zero margins
+ *   drr_volume_bounds        <- no counterpart: the occupied box and hull
+ *   drr_volume_hull             that let the walks skip exactly-zero margins
  *   drr_volume_pack          <- volume.py:77-79 flat_data() (the x-fastest
  *                               layout) + volume.py:196-222 import_raw's cast
  *                               and clamp, as one device pass
@@ -81,13 +81,21 @@ extern "C" {
  * which every voxel is exactly zero (drr_volume_bounds).  The walks then run
  * over that box only -- segments outside it add nothing to any sum, so every
  * image and gradient is bit-identical to the full walk.  All-zero occ_hi
- * means the whole volume. */
+ * means the whole volume.
+ * hull_valid / hull_lo / hull_hi (optional, with the box): drr_volume_hull's
+ * ranges of n . (i, j, k) over the non-zero voxels for the 10 diagonal
+ * directions n = (1,1,0) (1,-1,0) (1,0,1) (1,0,-1) (0,1,1) (0,1,-1)
+ * (1,1,1) (1,1,-1) (1,-1,1) (-1,1,1); each ray is then also trimmed to that
+ * polytope (again bit-identical). */
 typedef struct drr_grid {
   int64_t dims[3];
   double spacing[3];
   double origin[3];
   int64_t occ_lo[3];
   int64_t occ_hi[3];
+  int32_t hull_valid;
+  int32_t hull_lo[10];
+  int32_t hull_hi[10];
 } drr_grid;
 
 /* Detector: H x W pixels, pitch_x along W, pitch_y along H (geometry.py:71-97,
@@ -170,6 +178,13 @@ int drr_backward_jac(const double *d_jac, int32_t n_poses,
  * gives lo = hi = 0.  d_bounds: 6 int32 device ints (lo[3], hi[3]). */
 int drr_volume_bounds(const void *d_vol, int vol_dtype, const drr_grid *grid,
                       int32_t *d_bounds, void *stream);
+
+/* The occupied hull of a device volume: for the 10 diagonal directions of
+ * drr_grid, the min (d_hull[0..9]) and max (d_hull[10..19]) of n . (i, j, k)
+ * over the voxels that are not exactly zero (NaN counts).  d_hull: 20 int32
+ * device ints. */
+int drr_volume_hull(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                    int32_t *d_hull, void *stream);
 
 /* One-time ingest of a device volume into the walk's layout: x-fastest
  * (flat = i + nx (j + ny k), volume.py:77-79), dst_dtype DRR_VOL_F32 / F64.

@@ -81,16 +81,17 @@ def _device_volume(flat_data, dims, dev):
 
 
 def _bounds(vol, dims):
+    """(occupied box, hull) of a device volume (drr_volume_bounds / _hull)."""
     from .renderer import volume_bounds
     return volume_bounds(vol, _lib.make_grid(dims, (1.0, 1.0, 1.0), (0.0, 0.0, 0.0)),
-                         _lib.DRR_VOL_F64)
+                         _lib.DRR_VOL_F64, hull=True)
 
 
 def _prep(flat_data, dims, spacing, origin, source, pixels):
     dev = _device()
     pix = np.ascontiguousarray(np.atleast_2d(pixels), dtype=np.float64)
-    vol, occupied = _device_volume(flat_data, dims, dev)
-    grid = _lib.make_grid(dims, spacing, origin, occupied)
+    vol, (occupied, hull) = _device_volume(flat_data, dims, dev)
+    grid = _lib.make_grid(dims, spacing, origin, occupied, hull)
     src = _upload(np.asarray(source).reshape(3), dev)
     return dev, grid, vol, src, _upload(pix, dev), pix.shape[0]
 

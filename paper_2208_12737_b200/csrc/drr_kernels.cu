@@ -20,6 +20,7 @@
 // loss_kernels.cuh / pose_kernels.cuh hold the loss, pose-frame and
 // registration-update kernels of the batched loss_and_gradient chain.
 #include <cuda_runtime.h>
+#include <limits.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -597,6 +598,56 @@ __global__ void k_bounds_finish(int* out) {
   }
 }
 
+// The occupied hull: for each of the 10 diagonal directions n_q, the min / max
+// of n_q . (i, j, k) over the voxels that are not exactly zero (NaN counts),
+// by integer atomics (order-free, deterministic).  out: lo[10], hi[10].
+template <typename VT>
+__global__ void __launch_bounds__(256)
+    k_volume_hull(const VT* __restrict__ vol, const GridDev g, int* __restrict__ out) {
+  int lo[10], hi[10];
+#pragma unroll
+  for (int q = 0; q < 10; ++q) {
+    lo[q] = INT_MAX;
+    hi[q] = INT_MIN;
+  }
+  const int64_t n = g.total;
+  for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!(vol[f] == VT(0))) {
+      const int c[3] = {static_cast<int>(f % g.n[0]), static_cast<int>((f / g.n[0]) % g.n[1]),
+                        static_cast<int>(f / (static_cast<int64_t>(g.n[0]) * g.n[1]))};
+#pragma unroll
+      for (int q = 0; q < 10; ++q) {
+        const int v = hull_dir(q, 0) * c[0] + hull_dir(q, 1) * c[1] + hull_dir(q, 2) * c[2];
+        lo[q] = min(lo[q], v);
+        hi[q] = max(hi[q], v);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 10; ++q) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      lo[q] = min(lo[q], __shfl_xor_sync(0xffffffffu, lo[q], off));
+      hi[q] = max(hi[q], __shfl_xor_sync(0xffffffffu, hi[q], off));
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int q = 0; q < 10; ++q) {
+      atomicMin(out + q, lo[q]);
+      atomicMax(out + 10 + q, hi[q]);
+    }
+  }
+}
+
+__global__ void k_hull_init(int* out) {
+  if (threadIdx.x < 10) {
+    out[threadIdx.x] = INT_MAX;
+    out[10 + threadIdx.x] = INT_MIN;
+  }
+}
+
 // ------------------------------------------------------ discrete signature
 // Per pose, a 64-bit signature of every ray's traversal structure (SigVisitor:
 // labels, used set, voxels, exit selector; a missed ray hashes as a miss),
@@ -918,6 +969,21 @@ int make_grid(const drr_grid* in, drr::GridDev& g) {
     volatile double phi = static_cast<double>(hi) * in->spacing[a];
     g.tlo[a] = in->origin[a] + plo;
     g.thi[a] = in->origin[a] + phi;
+    g.isp[a] = static_cast<float>(1.0 / in->spacing[a]);
+  }
+  // the occupied hull (drr_volume_hull): n . (i, j, k) ranges of the non-zero
+  // voxels -> the supports of their boxes [i, i+1] x ..., widened by 1/16 voxel
+  g.hull = in->hull_valid != 0 && !whole;
+  for (int q = 0; q < 10; ++q) {
+    int pos = 0, neg = 0, l1 = 0;
+    for (int a = 0; a < 3; ++a) {
+      const int c = drr::hull_dir(q, a);
+      pos += c > 0 ? c : 0;
+      neg += c < 0 ? c : 0;
+      l1 += c > 0 ? c : -c;
+    }
+    g.hlo[q] = static_cast<float>(in->hull_lo[q] + neg) - 0.0625f * l1;
+    g.hhi[q] = static_cast<float>(in->hull_hi[q] + pos) + 0.0625f * l1;
   }
   if (table_bytes(g, true) > 227 * 1024)
     return fail(DRR_ERR_INVALID_ARGUMENT, "plane table of %zu bytes exceeds shared memory",
@@ -1419,6 +1485,26 @@ int drr_volume_bounds(const void* d_vol, int vol_dtype, const drr_grid* grid,
   return check_launch("drr_volume_bounds");
 }
 
+int drr_volume_hull(const void* d_vol, int vol_dtype, const drr_grid* grid, int32_t* d_hull,
+                    void* stream) {
+  drr::GridDev g;
+  const int rc = make_grid(grid, g);
+  if (rc) return rc;
+  if (d_vol == nullptr || d_hull == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "drr_volume_hull: NULL argument");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t blocks = (static_cast<int64_t>(g.total) + 255) / 256;
+  const unsigned grd = static_cast<unsigned>(blocks < 148 * 16 ? blocks : 148 * 16);
+  drr::k_hull_init<<<1, 32, 0, st>>>(d_hull);
+  if (vol_dtype == DRR_VOL_F32)
+    drr::k_volume_hull<float><<<grd, 256, 0, st>>>(static_cast<const float*>(d_vol), g, d_hull);
+  else if (vol_dtype == DRR_VOL_F64)
+    drr::k_volume_hull<double><<<grd, 256, 0, st>>>(static_cast<const double*>(d_vol), g, d_hull);
+  else
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
+  return check_launch("drr_volume_hull");
+}
+
 int drr_signature(const void* d_vol, int vol_dtype, const drr_grid* grid,
                   const double* d_frames, int32_t n_poses, const drr_detector* det,
                   uint64_t* d_sig, void* stream) {
@@ -1430,6 +1516,7 @@ int drr_signature(const void* d_vol, int vol_dtype, const drr_grid* grid,
     g.tlo[a] = g.o[a];
     g.thi[a] = g.hi[a];
   }
+  g.hull = 0;
   const size_t smem = table_bytes(g, false);
   rc = make_det(det, d);
   if (rc) return rc;

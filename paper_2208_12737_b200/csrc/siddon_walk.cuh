@@ -50,7 +50,27 @@ struct GridDev {
   // so the trimmed entry / exit parameters are the walk's own crossing
   // parameters of those planes; the whole volume gives tlo = o, thi = hi
   double tlo[3], thi[3];
+  // optional occupied hull (hull != 0): in voxel-index coordinates u_a =
+  // (x_a - o_a) / sp_a every voxel that is not exactly zero lies inside
+  // hlo[q] <= n_q . u <= hhi[q] for the 10 diagonal directions n_q of
+  // hull_dir (the box covers the axis directions); the supports are of the
+  // voxels' whole boxes, widened by 1/16 voxel against rounding (the fp32 slab
+  // tests err by ~1e-4 voxel, the reference's midpoints by ~1e-12)
+  int hull;
+  float isp[3];  // 1 / sp
+  float hlo[10], hhi[10];
 };
+// A/B (scripts/gpu_ab_trim.sh, 256 C2 poses): unrolled 10.70 ms, rolled 12.71
+// (its runtime direction table); box-only trimming 11.31 / 11.78.
+#ifndef DRR_HULL_UNROLL
+#define DRR_HULL_UNROLL 1
+#endif
+// Hull directions (integer components, voxel-index space).
+__host__ __device__ __forceinline__ int hull_dir(int q, int a) {
+  constexpr int kDir[10][3] = {{1, 1, 0}, {1, -1, 0}, {1, 0, 1}, {1, 0, -1}, {0, 1, 1},
+                               {0, 1, -1}, {1, 1, 1}, {1, 1, -1}, {1, -1, 1}, {-1, 1, 1}};
+  return kDir[q][a];
+}
 
 template <typename VT>
 __device__ __forceinline__ double load_voxel(const VT* __restrict__ vol, int i) {
@@ -246,6 +266,92 @@ __device__ __forceinline__ double axis_alpha(const GridDev& g, const Ray& r, int
   return plane_alpha(o, sp, k, s, d, inv, true);
 }
 
+// Trim [amin, amax] to the occupied hull (GridDev::hull), exactly.  fp32 slab
+// tests against the 10 hull directions give the approximate parameters where
+// the ray enters and leaves the hull; since the hull holds the non-zero
+// voxels' whole boxes (widened against rounding), everything the exact ray
+// meets before the entry -- midpoint rounding included -- is an exactly-zero
+// voxel.  The walk then starts at the last dominant-axis plane crossing at
+// least 1/16 voxel before the entry (its
+// exact parameter, the walk's own) with entry_exit's semantics (a virtual
+// crossing, then every crossing >= amin on every axis, ties to the lowest
+// axis), and stops symmetrically after the exit: the skipped segments add
+// +0 and the skipped crossings carry coefficient 0, so images and sums keep
+// the full walk's bits.  A ray that misses the hull is a miss (its full walk
+// sums zeros).
+__device__ __forceinline__ void hull_trim(const GridDev& g, Ray& r) {
+  float us[3], ud[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    us[a] = static_cast<float>((r.s[a] - g.o[a]) * static_cast<double>(g.isp[a]));
+    ud[a] = static_cast<float>(r.d[a] * static_cast<double>(g.isp[a]));
+  }
+  float tin = static_cast<float>(r.amin), tout = static_cast<float>(r.amax);
+#if DRR_HULL_UNROLL
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+  for (int q = 0; q < 10; ++q) {
+    float ns = 0.f, nd = 0.f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      ns += hull_dir(q, a) * us[a];
+      nd += hull_dir(q, a) * ud[a];
+    }
+    if (nd != 0.f) {
+      const float inv = 1.0f / nd;
+      const float t1 = (g.hlo[q] - ns) * inv, t2 = (g.hhi[q] - ns) * inv;
+      tin = fmaxf(tin, fminf(t1, t2));
+      tout = fminf(tout, fmaxf(t1, t2));
+    } else if (ns < g.hlo[q] || ns > g.hhi[q]) {
+      tin = 1.f;
+      tout = 0.f;
+    }
+  }
+  if (!(tin < tout)) {
+    r.hit = false;
+    return;
+  }
+  const int D = r.D;
+  const double udD = D == 0 ? ud[0] : (D == 1 ? ud[1] : ud[2]);
+  const double usD = D == 0 ? us[0] : (D == 1 ? us[1] : us[2]);
+  const int stD = udD > 0.0 ? 1 : -1;
+  const double half = 0.0625 / fabs(udD);  // 1/16 dominant-axis voxel, in alpha
+  const int nD = g.n[D];
+  if (static_cast<double>(tin) - half > r.amin) {
+    const double target = static_cast<double>(tin) - half;
+    const double u = usD + target * udD;
+    int k = static_cast<int>(stD > 0 ? floor(u) : ceil(u));  // last D-plane before target
+    k = k < 0 ? 0 : (k > nD ? nD : k);
+    double ak = axis_alpha(g, r, D, k);
+    if (!(ak < target)) {
+      k -= stD;
+      ak = (k >= 0 && k <= nD) ? axis_alpha(g, r, D, k) : r.amin;
+    }
+    if (ak > r.amin && ak < target) {
+      r.amin = ak;
+      r.lab_min = D;
+    }
+  }
+  if (static_cast<double>(tout) + half < r.amax) {
+    const double target = static_cast<double>(tout) + half;
+    const double u = usD + target * udD;
+    int k = static_cast<int>(stD > 0 ? ceil(u) : floor(u));  // first D-plane after target
+    k = k < 0 ? 0 : (k > nD ? nD : k);
+    double ak = axis_alpha(g, r, D, k);
+    if (!(ak > target)) {
+      k += stD;
+      ak = (k >= 0 && k <= nD) ? axis_alpha(g, r, D, k) : r.amax;
+    }
+    if (ak < r.amax && ak > target) {
+      r.amax = ak;
+      r.lab_max = D;
+    }
+  }
+  r.hit = r.amin < r.amax;
+}
+
 // Per-ray setup for chunk `chunk` of `nchunks` (one ray split
 // across threads by dominant-axis plane index ranges).  The crossing sequence
 // of the whole ray, ordered by (alpha, axis) like the reference's merge, is
@@ -292,6 +398,10 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
   }
   r.T = T;
   r.D = D;
+  if (g.hull) {
+    hull_trim(g, r);
+    if (!r.hit) return;
+  }
   // Start event per axis: (amin, entry) for chunk 0, else (alpha_D(b_j), D).
   double a_s = r.amin;
   int lab_s = -1;  // -1: entry semantics (every crossing with alpha >= amin)

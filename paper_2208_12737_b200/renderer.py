@@ -65,26 +65,50 @@ def pack_volume(src: torch.Tensor, dims, order: int, dtype=torch.float32,
     return out
 
 
-def volume_bounds(flat: torch.Tensor, grid, vol_dtype: int):
+def volume_bounds(flat: torch.Tensor, grid, vol_dtype: int, hull: bool = False):
     """``drr_volume_bounds``: ((lo0, lo1, lo2), (hi0, hi1, hi2)), the voxel box
-    outside of which the device volume is exactly zero (one sync)."""
-    out = torch.empty(6, dtype=torch.int32, device=flat.device)
-    _lib.check(_lib.load().drr_volume_bounds(flat.data_ptr(), vol_dtype, grid, out.data_ptr(),
-                                             _stream_ptr(flat.device)))
+    outside of which the device volume is exactly zero; with ``hull`` also
+    ``drr_volume_hull``'s (lo[10], hi[10]) (None for an all-zero volume).
+    One sync."""
+    out = torch.empty(26, dtype=torch.int32, device=flat.device)
+    lib = _lib.load()
+    _lib.check(lib.drr_volume_bounds(flat.data_ptr(), vol_dtype, grid, out.data_ptr(),
+                                     _stream_ptr(flat.device)))
+    if hull:
+        _lib.check(lib.drr_volume_hull(flat.data_ptr(), vol_dtype, grid, out[6:].data_ptr(),
+                                       _stream_ptr(flat.device)))
     b = [int(x) for x in out.cpu().tolist()]
-    return tuple(b[:3]), tuple(b[3:])
+    box = (tuple(b[:3]), tuple(b[3:6]))
+    if not hull:
+        return box
+    empty = box == ((0, 0, 0), (0, 0, 0))
+    return box, (None if empty else (tuple(b[6:16]), tuple(b[16:26])))
+
+
+def trim_grid(flat: torch.Tensor, dims, spacing, origin, vol_dtype: int, trim=True):
+    """(grid, occupied box, hull) for a device volume: ``trim`` True = the box
+    and the 10-direction hull, "box" = the box only, False = the whole volume."""
+    grid = _lib.make_grid(dims, spacing, origin)
+    if not trim or flat.numel() == 0:
+        return grid, None, None
+    box, hull = volume_bounds(flat, grid, vol_dtype, hull=True)
+    if trim == "box":
+        hull = None
+    return _lib.make_grid(dims, spacing, origin, box, hull), box, hull
 
 
 class DeviceVolume:
     """A CT volume resident in HBM: float32, x-fastest, plus its grid.
 
-    ``trim`` (default): the grid carries the volume's occupied box
-    (:func:`volume_bounds`) and the walks skip its exactly-zero margins --
-    bit-identical results, fewer voxel-steps (``refresh_bounds`` after
-    writing into ``flat``)."""
+    ``trim`` (default True): the grid carries the volume's occupied box and
+    hull (:func:`volume_bounds`); every ray is walked only between where it
+    enters and leaves them, so the exactly-zero margins are skipped --
+    bit-identical results, fewer voxel-steps.  ``trim="box"`` keeps the box
+    only, ``False`` walks the whole volume.  Call ``refresh_bounds`` after
+    writing into ``flat``."""
 
     def __init__(self, data, spacing, origin=(0.0, 0.0, 0.0), device=None,
-                 dtype=torch.float32, trim: bool = True):
+                 dtype=torch.float32, trim=True):
         spacing = tuple(float(s) for s in np.broadcast_to(np.asarray(spacing, dtype=np.float64), (3,)))
         origin = tuple(float(s) for s in np.broadcast_to(np.asarray(origin, dtype=np.float64), (3,)))
         if isinstance(data, torch.Tensor):
@@ -110,12 +134,10 @@ class DeviceVolume:
         self.refresh_bounds()
 
     def refresh_bounds(self):
-        """(Re)compute the grid: with ``trim``, the occupied box of ``flat``."""
-        self.grid = _lib.make_grid(self.dims, self.spacing, self.origin)
-        self.occupied = None
-        if getattr(self, "trim", False) and self.flat.numel():
-            self.occupied = volume_bounds(self.flat, self.grid, self.vol_dtype)
-            self.grid = _lib.make_grid(self.dims, self.spacing, self.origin, self.occupied)
+        """(Re)compute the grid: with ``trim``, the occupied box (and hull) of ``flat``."""
+        self.grid, self.occupied, self.hull = trim_grid(
+            self.flat, self.dims, self.spacing, self.origin, self.vol_dtype,
+            getattr(self, "trim", False))
         return self
 
     @property
@@ -125,7 +147,7 @@ class DeviceVolume:
 
     @classmethod
     def from_flat(cls, flat, dims, spacing, origin=(0.0, 0.0, 0.0), device=None,
-                  dtype=torch.float32, clamp_negative: bool = False, trim: bool = True):
+                  dtype=torch.float32, clamp_negative: bool = False, trim=True):
         """From an x-fastest flat array (the reference's ``flat_data()``, .dvol /
         raw payloads): uploaded as-is, cast (and clamped) by drr_volume_pack."""
         dims = tuple(int(n) for n in dims)
@@ -165,6 +187,7 @@ class DeviceVolume:
         self.vol_dtype = _lib.DRR_VOL_F32 if dtype == torch.float32 else _lib.DRR_VOL_F64
         self.trim = False  # contents unknown until filled: refresh_bounds(trim) then
         self.occupied = None
+        self.hull = None
         self.grid = _lib.make_grid(self.dims, self.spacing, self.origin)
         return self
 

@@ -16,9 +16,9 @@ from paper_2208_12737_b200 import (DRR, backward_frames, backward_from_jac, coun
 dev = torch.device("cuda")
 vol = synthetic.chest_phantom()
 drr = DRR(vol, (0.703125, 0.703125, 2.5), 300.0, 200, 3.6, device=dev, strict=False)
-if os.environ.get("DRR_KBENCH_TRIM"):  # A/B of the trimming modes: "box", "none"
+if os.environ.get("DRR_KBENCH_TRIM"):  # A/B of the trimming modes: "none", "box", "hull"
     from paper_2208_12737_b200 import DeviceVolume
-    mode = {"box": True, "none": False}[os.environ["DRR_KBENCH_TRIM"]]
+    mode = {"hull": True, "box": "box", "none": False}[os.environ["DRR_KBENCH_TRIM"]]
     drr.volume = DeviceVolume(vol, (0.703125, 0.703125, 2.5), device=dev, trim=mode)
 if os.environ.get("DRR_KBENCH_F64"):  # the CT held as float64 (same values)
     from paper_2208_12737_b200 import DeviceVolume

@@ -1,5 +1,6 @@
 """Exact empty-space trimming: the occupied box (drr_volume_bounds; GridDev
-tlo / thi).  The walks skip the exactly-zero margins of the volume, and every
+tlo / thi) and the 10-direction hull (drr_volume_hull; hull_trim).  The
+walks skip the exactly-zero margins of the volume and of each ray, and every
 output must be bit-identical to the reference's whole-volume walk -- images,
 ray Jacobians, re-walk gradients, fused loss gradients, explicit-ray
 energies -- at C2 scale (the chest phantom's air margins), on a ball in its
@@ -41,6 +42,24 @@ def test_bounds_match_numpy(cuda_device):
     assert empty.occupied == ((0, 0, 0), (0, 0, 0))
 
 
+def test_hull_matches_numpy(cuda_device):
+    from paper_2208_12737_b200 import DeviceVolume
+    from paper_2208_12737_b200.renderer import volume_bounds
+    rng = np.random.default_rng(3)
+    v = np.zeros((23, 17, 11))
+    idx = (rng.integers(0, 23, 9), rng.integers(0, 17, 9), rng.integers(0, 11, 9))
+    v[idx] = rng.random(9) + 0.5
+    v[22, 0, 10] = np.nan
+    dv = DeviceVolume(v, 1.0, device=cuda_device, trim=False)
+    box, hull = volume_bounds(dv.flat, dv.grid, dv.vol_dtype, hull=True)
+    dirs = np.array([[1, 1, 0], [1, -1, 0], [1, 0, 1], [1, 0, -1], [0, 1, 1], [0, 1, -1],
+                     [1, 1, 1], [1, 1, -1], [1, -1, 1], [-1, 1, 1]])
+    occ = np.argwhere(~(v == 0))
+    dots = occ @ dirs.T
+    assert hull == (tuple(int(x) for x in dots.min(0)), tuple(int(x) for x in dots.max(0)))
+    assert box == _np_bounds(v)
+
+
 def _pair(data, spacing, dev, dtype=torch.float32):
     from paper_2208_12737_b200 import DeviceVolume
     a = DeviceVolume(data, spacing, device=dev, dtype=dtype)
@@ -51,8 +70,8 @@ def _pair(data, spacing, dev, dtype=torch.float32):
 @pytest.mark.parametrize("kind", ["ball", "blobs"])
 def test_trim_bitwise_air_inside_box(cuda_device, kind):
     """Shapes with air inside their bounding box (and rays that miss it)."""
-    from paper_2208_12737_b200 import (Detector, backward_frames, pose_frames, render_frames,
-                                       render_frames_jac, synthetic)
+    from paper_2208_12737_b200 import (Detector, backward_frames, count_steps, pose_frames,
+                                       render_frames, render_frames_jac, synthetic)
     from paper_2208_12737_b200.registration import loss_and_gradient
     n = 64
     if kind == "ball":
@@ -65,15 +84,19 @@ def test_trim_bitwise_air_inside_box(cuda_device, kind):
             c = rng.integers(8, n - 8, 3)
             data[c[0] - 4:c[0] + 4, c[1] - 3:c[1] + 5, c[2] - 5:c[2] + 2] = rng.random() + 0.5
     tv, fv = _pair(data, 1.0, cuda_device)
+    from paper_2208_12737_b200 import DeviceVolume
+    bv = DeviceVolume(data, 1.0, device=cuda_device, trim="box")
     det = Detector(96, 80, 1.4, ray_split=1)
     eta = torch.tensor(synthetic.sample_poses((120.0, 0.7, 1.1, 0.2, 0, 0, 0),
                                               synthetic.NARROW_HALF_WIDTHS, 6, seed=5),
                        device=cuda_device)
     fr = pose_frames(eta, tv.center).detach()
     ib, jb = render_frames_jac(fv, det, fr)
-    ia, ja = render_frames_jac(tv, det, fr)
-    torch.testing.assert_close(ia, ib, rtol=0, atol=0)
-    torch.testing.assert_close(ja, jb, rtol=0, atol=0)
+    for vol in (tv, bv):
+        ia, ja = render_frames_jac(vol, det, fr)
+        torch.testing.assert_close(ia, ib, rtol=0, atol=0)
+        torch.testing.assert_close(ja, jb, rtol=0, atol=0)
+    assert count_steps(tv, det, fr).sum() < count_steps(bv, det, fr).sum()
     g = torch.randn((6, 96, 80), device=cuda_device)
     torch.testing.assert_close(backward_frames(tv, det, fr, g), backward_frames(fv, det, fr, g),
                                rtol=0, atol=0)
@@ -101,7 +124,7 @@ def test_trim_sources_inside_volume(cuda_device):
     e_t, s_t, p_t = backend_cuda.ray_endpoint_grad(flat, (48,) * 3, (1.0,) * 3, (0.0,) * 3, src, pix)
     w = flat.copy()  # writeable: uploaded per call; walked untrimmed here
     orig = backend_cuda._bounds
-    backend_cuda._bounds = lambda vol, dims: ((0, 0, 0), tuple(int(n) for n in dims))
+    backend_cuda._bounds = lambda vol, dims: (((0, 0, 0), tuple(int(n) for n in dims)), None)
     try:
         e_f, s_f, p_f = backend_cuda.ray_endpoint_grad(w, (48,) * 3, (1.0,) * 3, (0.0,) * 3, src,
                                                        pix)
