@@ -83,10 +83,11 @@ extern "C" {
  * image and gradient is bit-identical to the full walk.  All-zero occ_hi
  * means the whole volume.
  * hull_valid / hull_lo / hull_hi (optional, with the box): drr_volume_hull's
- * ranges of n . (i, j, k) over the non-zero voxels for the 10 diagonal
- * directions n = (1,1,0) (1,-1,0) (1,0,1) (1,0,-1) (0,1,1) (0,1,-1)
- * (1,1,1) (1,1,-1) (1,-1,1) (-1,1,1); each ray is then also trimmed to that
- * polytope (again bit-identical). */
+ * ranges of n . (i, j, k) over the non-zero voxels for its directions
+ * n = (1,1,0) (1,-1,0) (1,0,1) (1,0,-1) (0,1,1) (0,1,-1) (1,1,1) (1,1,-1)
+ * (1,-1,1) (-1,1,1) (2,1,0) (1,2,0) (2,-1,0) (1,-2,0); hull_valid = the
+ * number of directions filled (drr_volume_hull_dirs()), 0 = no hull.  Each
+ * ray is then also trimmed to that polytope (again bit-identical). */
 typedef struct drr_grid {
   int64_t dims[3];
   double spacing[3];
@@ -94,8 +95,8 @@ typedef struct drr_grid {
   int64_t occ_lo[3];
   int64_t occ_hi[3];
   int32_t hull_valid;
-  int32_t hull_lo[10];
-  int32_t hull_hi[10];
+  int32_t hull_lo[16];
+  int32_t hull_hi[16];
 } drr_grid;
 
 /* Detector: H x W pixels, pitch_x along W, pitch_y along H (geometry.py:71-97,
@@ -179,10 +180,11 @@ int drr_backward_jac(const double *d_jac, int32_t n_poses,
 int drr_volume_bounds(const void *d_vol, int vol_dtype, const drr_grid *grid,
                       int32_t *d_bounds, void *stream);
 
-/* The occupied hull of a device volume: for the 10 diagonal directions of
- * drr_grid, the min (d_hull[0..9]) and max (d_hull[10..19]) of n . (i, j, k)
- * over the voxels that are not exactly zero (NaN counts).  d_hull: 20 int32
- * device ints. */
+/* The occupied hull of a device volume: for the drr_volume_hull_dirs()
+ * directions of drr_grid, the min (d_hull[0..15]) and max (d_hull[16..31]) of
+ * n . (i, j, k) over the voxels that are not exactly zero (NaN counts).
+ * d_hull: 32 int32 device ints. */
+int drr_volume_hull_dirs(void);
 int drr_volume_hull(const void *d_vol, int vol_dtype, const drr_grid *grid,
                     int32_t *d_hull, void *stream);
 

@@ -39,6 +39,7 @@ EXPORTS = (
     "drr_count_steps",
     "drr_volume_pack",
     "drr_volume_bounds",
+    "drr_volume_hull_dirs",
     "drr_volume_hull",
     "drr_signature",
     "drr_pose_frames",
@@ -60,8 +61,8 @@ class DrrGrid(ctypes.Structure):
                 ("occ_lo", ctypes.c_int64 * 3),
                 ("occ_hi", ctypes.c_int64 * 3),
                 ("hull_valid", ctypes.c_int32),
-                ("hull_lo", ctypes.c_int32 * 10),
-                ("hull_hi", ctypes.c_int32 * 10)]
+                ("hull_lo", ctypes.c_int32 * 16),
+                ("hull_hi", ctypes.c_int32 * 16)]
 
 
 class DrrRegConfig(ctypes.Structure):
@@ -106,6 +107,7 @@ _SIGNATURES = {
     "drr_backward_jac": ([_vp, _i32, _DP, _vp, _int, _vp, _vp, _sz, _vp], _int),
     "drr_count_steps": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
     "drr_volume_pack": ([_vp, _int, _int, ctypes.POINTER(_i64), _int, _vp, _int, _vp], _int),
+    "drr_volume_hull_dirs": ([], _int),
     "drr_volume_hull": ([_vp, _int, _GP, _vp, _vp], _int),
     "drr_volume_bounds": ([_vp, _int, _GP, _vp, _vp], _int),
     "drr_signature": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
@@ -166,11 +168,11 @@ def check(rc: int) -> None:
 def make_grid(dims, spacing, origin, occupied=None, hull=None) -> DrrGrid:
     """The C grid; ``occupied`` = ((lo0, lo1, lo2), (hi0, hi1, hi2)), the voxel
     box outside of which the volume is exactly zero (None: the whole volume);
-    ``hull`` = (lo[10], hi[10]) from drr_volume_hull (None: box only)."""
+    ``hull`` = (lo[n], hi[n]) from drr_volume_hull (None: box only)."""
     g = DrrGrid()
     if hull is not None:
-        g.hull_valid = 1
-        for q in range(10):
+        g.hull_valid = len(hull[0])
+        for q in range(len(hull[0])):
             g.hull_lo[q] = int(hull[0][q])
             g.hull_hi[q] = int(hull[1][q])
     for a in range(3):

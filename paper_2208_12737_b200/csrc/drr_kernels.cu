@@ -598,15 +598,16 @@ __global__ void k_bounds_finish(int* out) {
   }
 }
 
-// The occupied hull: for each of the 10 diagonal directions n_q, the min / max
+// The occupied hull: for each of the kHullDirs directions n_q, the min / max
 // of n_q . (i, j, k) over the voxels that are not exactly zero (NaN counts),
-// by integer atomics (order-free, deterministic).  out: lo[10], hi[10].
+// by integer atomics (order-free, deterministic).  out: lo[16], hi[16]
+// (the first kHullDirs of each used).
 template <typename VT>
 __global__ void __launch_bounds__(256)
     k_volume_hull(const VT* __restrict__ vol, const GridDev g, int* __restrict__ out) {
-  int lo[10], hi[10];
+  int lo[kHullDirs], hi[kHullDirs];
 #pragma unroll
-  for (int q = 0; q < 10; ++q) {
+  for (int q = 0; q < kHullDirs; ++q) {
     lo[q] = INT_MAX;
     hi[q] = INT_MIN;
   }
@@ -617,7 +618,7 @@ __global__ void __launch_bounds__(256)
       const int c[3] = {static_cast<int>(f % g.n[0]), static_cast<int>((f / g.n[0]) % g.n[1]),
                         static_cast<int>(f / (static_cast<int64_t>(g.n[0]) * g.n[1]))};
 #pragma unroll
-      for (int q = 0; q < 10; ++q) {
+      for (int q = 0; q < kHullDirs; ++q) {
         const int v = hull_dir(q, 0) * c[0] + hull_dir(q, 1) * c[1] + hull_dir(q, 2) * c[2];
         lo[q] = min(lo[q], v);
         hi[q] = max(hi[q], v);
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(256)
     }
   }
 #pragma unroll
-  for (int q = 0; q < 10; ++q) {
+  for (int q = 0; q < kHullDirs; ++q) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       lo[q] = min(lo[q], __shfl_xor_sync(0xffffffffu, lo[q], off));
@@ -634,17 +635,17 @@ __global__ void __launch_bounds__(256)
   }
   if ((threadIdx.x & 31) == 0) {
 #pragma unroll
-    for (int q = 0; q < 10; ++q) {
+    for (int q = 0; q < kHullDirs; ++q) {
       atomicMin(out + q, lo[q]);
-      atomicMax(out + 10 + q, hi[q]);
+      atomicMax(out + 16 + q, hi[q]);
     }
   }
 }
 
 __global__ void k_hull_init(int* out) {
-  if (threadIdx.x < 10) {
+  if (threadIdx.x < 16) {
     out[threadIdx.x] = INT_MAX;
-    out[10 + threadIdx.x] = INT_MIN;
+    out[16 + threadIdx.x] = INT_MIN;
   }
 }
 
@@ -973,8 +974,8 @@ int make_grid(const drr_grid* in, drr::GridDev& g) {
   }
   // the occupied hull (drr_volume_hull): n . (i, j, k) ranges of the non-zero
   // voxels -> the supports of their boxes [i, i+1] x ..., widened by 1/16 voxel
-  g.hull = in->hull_valid != 0 && !whole;
-  for (int q = 0; q < 10; ++q) {
+  g.hull = in->hull_valid == drr::kHullDirs && !whole;
+  for (int q = 0; q < drr::kHullDirs; ++q) {
     int pos = 0, neg = 0, l1 = 0;
     for (int a = 0; a < 3; ++a) {
       const int c = drr::hull_dir(q, a);
@@ -1484,6 +1485,8 @@ int drr_volume_bounds(const void* d_vol, int vol_dtype, const drr_grid* grid,
   drr::k_bounds_finish<<<1, 32, 0, st>>>(d_bounds);
   return check_launch("drr_volume_bounds");
 }
+
+int drr_volume_hull_dirs(void) { return drr::kHullDirs; }
 
 int drr_volume_hull(const void* d_vol, int vol_dtype, const drr_grid* grid, int32_t* d_hull,
                     void* stream) {

@@ -52,23 +52,32 @@ struct GridDev {
   double tlo[3], thi[3];
   // optional occupied hull (hull != 0): in voxel-index coordinates u_a =
   // (x_a - o_a) / sp_a every voxel that is not exactly zero lies inside
-  // hlo[q] <= n_q . u <= hhi[q] for the 10 diagonal directions n_q of
+  // hlo[q] <= n_q . u <= hhi[q] for the kHullDirs directions n_q of
   // hull_dir (the box covers the axis directions); the supports are of the
   // voxels' whole boxes, widened by 1/16 voxel against rounding (the fp32 slab
   // tests err by ~1e-4 voxel, the reference's midpoints by ~1e-12)
   int hull;
   float isp[3];  // 1 / sp
-  float hlo[10], hhi[10];
+  float hlo[16], hhi[16];
 };
 // A/B (scripts/gpu_ab_trim.sh, 256 C2 poses): unrolled 10.70 ms, rolled 12.71
 // (its runtime direction table); box-only trimming 11.31 / 11.78.
 #ifndef DRR_HULL_UNROLL
 #define DRR_HULL_UNROLL 1
 #endif
-// Hull directions (integer components, voxel-index space).
+// Hull directions (integer components, voxel-index space): the 10 diagonals
+// of the cube, then 4 in-plane (x, y) directions that round the octagonal
+// cross-section to a 16-gon (a patient's body is a prism along z).  The ABI
+// carries 16 slots (drr_grid::hull_lo / hull_hi).
+#ifndef DRR_HULL_DIRS
+#define DRR_HULL_DIRS 14
+#endif
+constexpr int kHullDirs = DRR_HULL_DIRS;
 __host__ __device__ __forceinline__ int hull_dir(int q, int a) {
-  constexpr int kDir[10][3] = {{1, 1, 0}, {1, -1, 0}, {1, 0, 1}, {1, 0, -1}, {0, 1, 1},
-                               {0, 1, -1}, {1, 1, 1}, {1, 1, -1}, {1, -1, 1}, {-1, 1, 1}};
+  constexpr int kDir[16][3] = {{1, 1, 0}, {1, -1, 0}, {1, 0, 1}, {1, 0, -1}, {0, 1, 1},
+                               {0, 1, -1}, {1, 1, 1}, {1, 1, -1}, {1, -1, 1}, {-1, 1, 1},
+                               {2, 1, 0}, {1, 2, 0}, {2, -1, 0}, {1, -2, 0},
+                               {0, 0, 0}, {0, 0, 0}};
   return kDir[q][a];
 }
 
@@ -267,7 +276,7 @@ __device__ __forceinline__ double axis_alpha(const GridDev& g, const Ray& r, int
 }
 
 // Trim [amin, amax] to the occupied hull (GridDev::hull), exactly.  fp32 slab
-// tests against the 10 hull directions give the approximate parameters where
+// tests against the kHullDirs hull directions give the approximate parameters where
 // the ray enters and leaves the hull; since the hull holds the non-zero
 // voxels' whole boxes (widened against rounding), everything the exact ray
 // meets before the entry -- midpoint rounding included -- is an exactly-zero
@@ -292,7 +301,7 @@ __device__ __forceinline__ void hull_trim(const GridDev& g, Ray& r) {
 #else
 #pragma unroll 1
 #endif
-  for (int q = 0; q < 10; ++q) {
+  for (int q = 0; q < kHullDirs; ++q) {
     float ns = 0.f, nd = 0.f;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {

@@ -68,9 +68,9 @@ def pack_volume(src: torch.Tensor, dims, order: int, dtype=torch.float32,
 def volume_bounds(flat: torch.Tensor, grid, vol_dtype: int, hull: bool = False):
     """``drr_volume_bounds``: ((lo0, lo1, lo2), (hi0, hi1, hi2)), the voxel box
     outside of which the device volume is exactly zero; with ``hull`` also
-    ``drr_volume_hull``'s (lo[10], hi[10]) (None for an all-zero volume).
+    ``drr_volume_hull``'s (lo[n], hi[n]) (None for an all-zero volume).
     One sync."""
-    out = torch.empty(26, dtype=torch.int32, device=flat.device)
+    out = torch.empty(6 + 32, dtype=torch.int32, device=flat.device)
     lib = _lib.load()
     _lib.check(lib.drr_volume_bounds(flat.data_ptr(), vol_dtype, grid, out.data_ptr(),
                                      _stream_ptr(flat.device)))
@@ -81,8 +81,9 @@ def volume_bounds(flat: torch.Tensor, grid, vol_dtype: int, hull: bool = False):
     box = (tuple(b[:3]), tuple(b[3:6]))
     if not hull:
         return box
+    nd = lib.drr_volume_hull_dirs()
     empty = box == ((0, 0, 0), (0, 0, 0))
-    return box, (None if empty else (tuple(b[6:16]), tuple(b[16:26])))
+    return box, (None if empty else (tuple(b[6:6 + nd]), tuple(b[22:22 + nd])))
 
 
 def trim_grid(flat: torch.Tensor, dims, spacing, origin, vol_dtype: int, trim=True):

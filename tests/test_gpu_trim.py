@@ -53,7 +53,8 @@ def test_hull_matches_numpy(cuda_device):
     dv = DeviceVolume(v, 1.0, device=cuda_device, trim=False)
     box, hull = volume_bounds(dv.flat, dv.grid, dv.vol_dtype, hull=True)
     dirs = np.array([[1, 1, 0], [1, -1, 0], [1, 0, 1], [1, 0, -1], [0, 1, 1], [0, 1, -1],
-                     [1, 1, 1], [1, 1, -1], [1, -1, 1], [-1, 1, 1]])
+                     [1, 1, 1], [1, 1, -1], [1, -1, 1], [-1, 1, 1],
+                     [2, 1, 0], [1, 2, 0], [2, -1, 0], [1, -2, 0]])
     occ = np.argwhere(~(v == 0))
     dots = occ @ dirs.T
     assert hull == (tuple(int(x) for x in dots.min(0)), tuple(int(x) for x in dots.max(0)))
