@@ -42,6 +42,8 @@
  *                               walk per ray, no stored Jacobian
  *   drr_register_update      <- one iteration of registration.py:89-125
  *                               register() (momentum GD + convergence state)
+ *   drr_register_step        <- the same iteration with its loss and
+ *                               gradient: three launches in all
  *   drr_volume_bounds        <- no counterpart: the occupied box and hull
  *   drr_volume_hull             that let the walks skip exactly-zero margins
  *   drr_volume_pack          <- volume.py:77-79 flat_data() (the x-fastest
@@ -299,6 +301,24 @@ typedef struct drr_peer_handle {
 int drr_peer_export(const void *d_ptr, drr_peer_handle *out);
 int drr_peer_open(const drr_peer_handle *h, void **d_ptr);
 int drr_peer_close(void *d_ptr, uint64_t offset);
+
+/* One momentum-GD iteration `iter` for B registrations in three launches: the
+ * Jacobian-free walk of drr_forward_loss_grad at d_frames, the loss, and a
+ * reduction that also applies drr_register_update's bookkeeping and step and
+ * writes the frames of the updated poses back into d_frames for the next
+ * iteration (isocenter: 3 doubles in HOST memory).  d_frames must hold the
+ * frames of d_eta on entry (drr_pose_frames once before the first
+ * iteration).  Workspace: drr_loss_grad_workspace_size. */
+int drr_register_step(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                      double *d_frames, double *d_eta, double *d_velocity,
+                      int32_t n_poses, const drr_detector *det,
+                      const void *d_fixed, int64_t fixed_stride, int kind,
+                      void *d_img, int img_dtype, double *d_value,
+                      int *d_status, const double *isocenter,
+                      const drr_reg_config *cfg, int32_t iter, int *d_state,
+                      int *d_n_records, double *d_trace_eta,
+                      double *d_trace_loss, void *d_workspace,
+                      size_t workspace_bytes, void *stream);
 
 #ifdef __cplusplus
 }

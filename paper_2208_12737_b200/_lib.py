@@ -46,6 +46,7 @@ EXPORTS = (
     "drr_pose_grad",
     "drr_image_loss",
     "drr_register_update",
+    "drr_register_step",
     "drr_loss_grad_workspace_size",
     "drr_forward_loss_grad",
     "drr_peer_export",
@@ -119,6 +120,9 @@ _SIGNATURES = {
     "drr_loss_grad_workspace_size": ([_i32, _DP], _sz),
     "drr_forward_loss_grad": ([_vp, _int, _GP, _vp, _vp, _i32, _DP, _vp, _i64, _int, _vp, _int,
                                _vp, _vp, _vp, _vp, _vp, _sz, _vp], _int),
+    "drr_register_step": ([_vp, _int, _GP, _vp, _vp, _vp, _i32, _DP, _vp, _i64, _int, _vp, _int,
+                           _vp, _vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(DrrRegConfig),
+                           _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp], _int),
     "drr_peer_export": ([_vp, ctypes.POINTER(DrrPeerHandle)], _int),
     "drr_peer_open": ([ctypes.POINTER(DrrPeerHandle), ctypes.POINTER(_vp)], _int),
     "drr_peer_close": ([_vp, ctypes.c_uint64], _int),

@@ -695,10 +695,31 @@ __global__ void __launch_bounds__(kThreads)
 // has ~1250 small tiles; this keeps its reduction off the latency path.
 constexpr int kReduceRows = 8;
 constexpr int kReduceLossThreads = kReduceRows * kLossSums;  // 288
+// With `reg.on`, the same kernel is also one registration iteration
+// (registration.py:89-125): thread 0 applies register_update_one with this
+// pose's dL/dframe and writes the frame of the updated pose for the next walk,
+// so a whole iteration is three launches (walk, loss, this).
+struct RegStep {
+  int on;
+  int iter;
+  RegConfig cfg;
+  double* eta;
+  double* vel;
+  const double* value;
+  const int* status;
+  int* state;
+  int* n_rec;
+  double* trace_eta;
+  double* trace_loss;
+  double* frames;  // next frames (the walk of the next iteration reads them)
+  double iso0, iso1, iso2;
+};
+
 __global__ void __launch_bounds__(kReduceLossThreads)
     k_reduce_loss_grad(const double* __restrict__ partials, int blocks_per_pose,
                        const double* __restrict__ coef, const double* __restrict__ eta,
-                       double* __restrict__ grad_frames, double* __restrict__ grad_eta) {
+                       double* __restrict__ grad_frames, double* __restrict__ grad_eta,
+                       RegStep reg) {
   const int b = blockIdx.x;
   const int k = threadIdx.x % kLossSums, r = threadIdx.x / kLossSums;
   __shared__ double sm[kReduceRows][kLossSums];
@@ -733,6 +754,11 @@ __global__ void __launch_bounds__(kReduceLossThreads)
     pose_grad(eta + 7 * b, gf, ge);
 #pragma unroll
     for (int q = 0; q < 7; ++q) grad_eta[7 * b + q] = ge[q];
+  }
+  if (threadIdx.x == 0 && reg.on) {
+    if (register_update_one(b, reg.eta, reg.vel, gf, reg.value[b], reg.status[b], reg.cfg,
+                            reg.iter, reg.state, reg.n_rec, reg.trace_eta, reg.trace_loss))
+      pose_frame_one(reg.eta + 7 * b, reg.iso0, reg.iso1, reg.iso2, reg.frames + 12 * b);
   }
 }
 
@@ -1144,6 +1170,89 @@ void dispatch_pack(const void* src, int src_type, int order, const int64_t* dims
 }
 }  // namespace
 
+static int loss_step(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                     const double* d_frames, const double* d_eta, int32_t n_poses,
+                     const drr_detector* det, const void* d_fixed, int64_t fixed_stride, int kind,
+                     void* d_img, int img_dtype, double* d_value, int* d_status,
+                     double* d_grad_frames, double* d_grad_eta, void* d_workspace,
+                     size_t workspace_bytes, void* stream, const drr::RegStep& reg) {
+  drr::GridDev g;
+  drr::DetDev d;
+  int rc = make_grid(grid, g);
+  if (rc) return rc;
+  const size_t smem = table_bytes(g, true);
+  rc = make_det(det, d);
+  if (rc) return rc;
+  if (n_poses < 0 || n_poses > 65535)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
+  if (n_poses == 0) return DRR_OK;
+  if (kind != DRR_LOSS_NEG_ZNCC && kind != DRR_LOSS_L2)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "loss kind must be neg_zncc (0) or l2 (1), got %d", kind);
+  const int64_t npix = static_cast<int64_t>(d.H) * d.W;
+  if (fixed_stride != 0 && fixed_stride != npix)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "fixed_stride must be 0 or H*W");
+  if (d_img == nullptr || d_fixed == nullptr || d_value == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "d_img, d_fixed and d_value must not be NULL");
+  if (d_grad_eta != nullptr && d_eta == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "d_grad_eta needs d_eta");
+  if ((vol_dtype != DRR_VOL_F32 && vol_dtype != DRR_VOL_F64) || (img_dtype != 0 && img_dtype != 1))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "bad dtypes vol=%d img=%d", vol_dtype, img_dtype);
+  const size_t need = drr_loss_grad_workspace_size(n_poses, det);
+  if (workspace_bytes < need || d_workspace == nullptr)
+    return fail(DRR_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int K = ray_split(d, n_poses);
+  const dim3 grd = pose_grid(d, n_poses, K);
+  const int tiles = static_cast<int>(grd.x * grd.y);
+  double* partials = static_cast<double*>(d_workspace);
+  double* coef = partials + static_cast<size_t>(n_poses) * tiles * drr::kLossSums;
+  DRR_DISPATCH_K(K,
+    if (vol_dtype == DRR_VOL_F32 && img_dtype == 0) {
+      ensure_smem(drr::k_forward_loss<float, float, kK>, smem);
+      drr::k_forward_loss<float, float, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const float*>(d_vol), g, d_frames, d, static_cast<float*>(d_img),
+          static_cast<const float*>(d_fixed), fixed_stride, partials);
+    } else if (vol_dtype == DRR_VOL_F32) {
+      ensure_smem(drr::k_forward_loss<float, double, kK>, smem);
+      drr::k_forward_loss<float, double, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const float*>(d_vol), g, d_frames, d, static_cast<double*>(d_img),
+          static_cast<const double*>(d_fixed), fixed_stride, partials);
+    } else if (img_dtype == 1) {
+      ensure_smem(drr::k_forward_loss<double, double, kK>, smem);
+      drr::k_forward_loss<double, double, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const double*>(d_vol), g, d_frames, d, static_cast<double*>(d_img),
+          static_cast<const double*>(d_fixed), fixed_stride, partials);
+    } else {
+      ensure_smem(drr::k_forward_loss<double, float, kK>, smem);
+      drr::k_forward_loss<double, float, kK><<<grd, drr::kThreads, smem, st>>>(
+          static_cast<const double*>(d_vol), g, d_frames, d, static_cast<float*>(d_img),
+          static_cast<const float*>(d_fixed), fixed_stride, partials);
+    })
+  rc = check_launch("drr_forward_loss_grad/walk");
+  if (rc) return rc;
+  for (int32_t i0 = 0; i0 < n_poses; i0 += 65535) {
+    const int32_t n = n_poses - i0 < 65535 ? n_poses - i0 : 65535;
+    const dim3 lg(drr::kLossCluster, n);
+    const int64_t fo = fixed_stride * i0, io = npix * i0;
+    int* sts = d_status ? d_status + i0 : nullptr;
+    if (img_dtype == 0)
+      drr::k_image_loss<float><<<lg, drr::kLossThreads, 0, st>>>(
+          static_cast<const float*>(d_img) + io, static_cast<const float*>(d_fixed) + fo,
+          fixed_stride, npix, kind, d_value + i0, nullptr, sts, coef + 3 * i0);
+    else
+      drr::k_image_loss<double><<<lg, drr::kLossThreads, 0, st>>>(
+          static_cast<const double*>(d_img) + io, static_cast<const double*>(d_fixed) + fo,
+          fixed_stride, npix, kind, d_value + i0, nullptr, sts, coef + 3 * i0);
+    rc = check_launch("drr_forward_loss_grad/loss");
+    if (rc) return rc;
+  }
+  if (d_grad_frames == nullptr && d_grad_eta == nullptr && !reg.on) return DRR_OK;
+  drr::k_reduce_loss_grad<<<n_poses, drr::kReduceLossThreads, 0, st>>>(
+      partials, tiles, coef, d_eta, d_grad_frames, d_grad_eta, reg);
+  return check_launch("drr_forward_loss_grad/reduce");
+}
+
+
 extern "C" {
 
 const char* drr_last_error(void) { return g_err; }
@@ -1388,80 +1497,53 @@ int drr_forward_loss_grad(const void* d_vol, int vol_dtype, const drr_grid* grid
                           int kind, void* d_img, int img_dtype, double* d_value, int* d_status,
                           double* d_grad_frames, double* d_grad_eta, void* d_workspace,
                           size_t workspace_bytes, void* stream) {
-  drr::GridDev g;
-  drr::DetDev d;
-  int rc = make_grid(grid, g);
-  if (rc) return rc;
-  const size_t smem = table_bytes(g, true);
-  rc = make_det(det, d);
-  if (rc) return rc;
-  if (n_poses < 0 || n_poses > 65535)
-    return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
-  if (n_poses == 0) return DRR_OK;
-  if (kind != DRR_LOSS_NEG_ZNCC && kind != DRR_LOSS_L2)
-    return fail(DRR_ERR_INVALID_ARGUMENT, "loss kind must be neg_zncc (0) or l2 (1), got %d", kind);
-  const int64_t npix = static_cast<int64_t>(d.H) * d.W;
-  if (fixed_stride != 0 && fixed_stride != npix)
-    return fail(DRR_ERR_INVALID_ARGUMENT, "fixed_stride must be 0 or H*W");
-  if (d_img == nullptr || d_fixed == nullptr || d_value == nullptr)
-    return fail(DRR_ERR_INVALID_ARGUMENT, "d_img, d_fixed and d_value must not be NULL");
-  if (d_grad_eta != nullptr && d_eta == nullptr)
-    return fail(DRR_ERR_INVALID_ARGUMENT, "d_grad_eta needs d_eta");
-  if ((vol_dtype != DRR_VOL_F32 && vol_dtype != DRR_VOL_F64) || (img_dtype != 0 && img_dtype != 1))
-    return fail(DRR_ERR_INVALID_ARGUMENT, "bad dtypes vol=%d img=%d", vol_dtype, img_dtype);
-  const size_t need = drr_loss_grad_workspace_size(n_poses, det);
-  if (workspace_bytes < need || d_workspace == nullptr)
-    return fail(DRR_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
-  const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int K = ray_split(d, n_poses);
-  const dim3 grd = pose_grid(d, n_poses, K);
-  const int tiles = static_cast<int>(grd.x * grd.y);
-  double* partials = static_cast<double*>(d_workspace);
-  double* coef = partials + static_cast<size_t>(n_poses) * tiles * drr::kLossSums;
-  DRR_DISPATCH_K(K,
-    if (vol_dtype == DRR_VOL_F32 && img_dtype == 0) {
-      ensure_smem(drr::k_forward_loss<float, float, kK>, smem);
-      drr::k_forward_loss<float, float, kK><<<grd, drr::kThreads, smem, st>>>(
-          static_cast<const float*>(d_vol), g, d_frames, d, static_cast<float*>(d_img),
-          static_cast<const float*>(d_fixed), fixed_stride, partials);
-    } else if (vol_dtype == DRR_VOL_F32) {
-      ensure_smem(drr::k_forward_loss<float, double, kK>, smem);
-      drr::k_forward_loss<float, double, kK><<<grd, drr::kThreads, smem, st>>>(
-          static_cast<const float*>(d_vol), g, d_frames, d, static_cast<double*>(d_img),
-          static_cast<const double*>(d_fixed), fixed_stride, partials);
-    } else if (img_dtype == 1) {
-      ensure_smem(drr::k_forward_loss<double, double, kK>, smem);
-      drr::k_forward_loss<double, double, kK><<<grd, drr::kThreads, smem, st>>>(
-          static_cast<const double*>(d_vol), g, d_frames, d, static_cast<double*>(d_img),
-          static_cast<const double*>(d_fixed), fixed_stride, partials);
-    } else {
-      ensure_smem(drr::k_forward_loss<double, float, kK>, smem);
-      drr::k_forward_loss<double, float, kK><<<grd, drr::kThreads, smem, st>>>(
-          static_cast<const double*>(d_vol), g, d_frames, d, static_cast<float*>(d_img),
-          static_cast<const float*>(d_fixed), fixed_stride, partials);
-    })
-  rc = check_launch("drr_forward_loss_grad/walk");
-  if (rc) return rc;
-  for (int32_t i0 = 0; i0 < n_poses; i0 += 65535) {
-    const int32_t n = n_poses - i0 < 65535 ? n_poses - i0 : 65535;
-    const dim3 lg(drr::kLossCluster, n);
-    const int64_t fo = fixed_stride * i0, io = npix * i0;
-    int* sts = d_status ? d_status + i0 : nullptr;
-    if (img_dtype == 0)
-      drr::k_image_loss<float><<<lg, drr::kLossThreads, 0, st>>>(
-          static_cast<const float*>(d_img) + io, static_cast<const float*>(d_fixed) + fo,
-          fixed_stride, npix, kind, d_value + i0, nullptr, sts, coef + 3 * i0);
-    else
-      drr::k_image_loss<double><<<lg, drr::kLossThreads, 0, st>>>(
-          static_cast<const double*>(d_img) + io, static_cast<const double*>(d_fixed) + fo,
-          fixed_stride, npix, kind, d_value + i0, nullptr, sts, coef + 3 * i0);
-    rc = check_launch("drr_forward_loss_grad/loss");
-    if (rc) return rc;
-  }
-  if (d_grad_frames == nullptr && d_grad_eta == nullptr) return DRR_OK;
-  drr::k_reduce_loss_grad<<<n_poses, drr::kReduceLossThreads, 0, st>>>(
-      partials, tiles, coef, d_eta, d_grad_frames, d_grad_eta);
-  return check_launch("drr_forward_loss_grad/reduce");
+  drr::RegStep off{};
+  off.on = 0;
+  return loss_step(d_vol, vol_dtype, grid, d_frames, d_eta, n_poses, det, d_fixed, fixed_stride,
+                   kind, d_img, img_dtype, d_value, d_status, d_grad_frames, d_grad_eta,
+                   d_workspace, workspace_bytes, stream, off);
+}
+
+int drr_register_step(const void* d_vol, int vol_dtype, const drr_grid* grid, double* d_frames,
+                      double* d_eta, double* d_velocity, int32_t n_poses, const drr_detector* det,
+                      const void* d_fixed, int64_t fixed_stride, int kind, void* d_img,
+                      int img_dtype, double* d_value, int* d_status, const double* isocenter,
+                      const drr_reg_config* cfg, int32_t iter, int* d_state, int* d_n_records,
+                      double* d_trace_eta, double* d_trace_loss, void* d_workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (cfg == nullptr || isocenter == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "cfg and isocenter must not be NULL");
+  if (!(cfg->lr_rotation > 0) || !(cfg->lr_translation > 0))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "learning rates must be positive");
+  if (!(cfg->momentum >= 0.0 && cfg->momentum < 1.0))
+    return fail(DRR_ERR_INVALID_ARGUMENT, "momentum must be in [0, 1), got %g", cfg->momentum);
+  if (cfg->max_iters < 1)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "max_iters must be >= 1, got %d", cfg->max_iters);
+  if (iter < 0 || iter > cfg->max_iters)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "iter %d outside [0, max_iters]", iter);
+  if (d_status == nullptr || d_eta == nullptr || d_velocity == nullptr || d_state == nullptr ||
+      d_n_records == nullptr || d_trace_eta == nullptr || d_trace_loss == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "registration buffers must not be NULL");
+  drr::RegStep reg{};
+  reg.on = 1;
+  reg.iter = iter;
+  reg.cfg = drr::RegConfig{cfg->lr_rotation, cfg->lr_translation, cfg->momentum,
+                           cfg->converged_threshold, cfg->max_iters};
+  reg.eta = d_eta;
+  reg.vel = d_velocity;
+  reg.value = d_value;
+  reg.status = d_status;
+  reg.state = d_state;
+  reg.n_rec = d_n_records;
+  reg.trace_eta = d_trace_eta;
+  reg.trace_loss = d_trace_loss;
+  reg.frames = d_frames;
+  reg.iso0 = isocenter[0];
+  reg.iso1 = isocenter[1];
+  reg.iso2 = isocenter[2];
+  return loss_step(d_vol, vol_dtype, grid, d_frames, d_eta, n_poses, det, d_fixed, fixed_stride,
+                   kind, d_img, img_dtype, d_value, d_status, nullptr, nullptr, d_workspace,
+                   workspace_bytes, stream, reg);
 }
 
 int drr_volume_bounds(const void* d_vol, int vol_dtype, const drr_grid* grid,

@@ -28,18 +28,15 @@ __device__ __forceinline__ PoseTrig pose_trig(const double* eta) {
   return t;
 }
 
-__global__ void k_pose_frames(const double* __restrict__ eta, double iso0, double iso1,
-                              double iso2, int n, double* __restrict__ frames) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= n) return;
-  const double* e = eta + 7 * b;
+// The frame of one pose (geometry.py:120-149 + the isocenter offset).
+__device__ __forceinline__ void pose_frame_one(const double* __restrict__ e, double iso0,
+                                               double iso1, double iso2, double* __restrict__ f) {
   const PoseTrig t = pose_trig(e);
   const double rho = e[0];
   const double u[3] = {t.sp * t.ct, t.sp * t.st, t.cp};
   const double et[3] = {-t.st, t.ct, 0.0};
   const double ep[3] = {t.cp * t.ct, t.cp * t.st, -t.sp};
   const double iso[3] = {iso0, iso1, iso2};
-  double* f = frames + 12 * b;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     f[a] = iso[a] + (e[4 + a] + rho * u[a]);
@@ -47,6 +44,13 @@ __global__ void k_pose_frames(const double* __restrict__ eta, double iso0, doubl
     f[6 + a] = t.cg * ep[a] - t.sg * et[a];
     f[9 + a] = t.cg * et[a] + t.sg * ep[a];
   }
+}
+
+__global__ void k_pose_frames(const double* __restrict__ eta, double iso0, double iso1,
+                              double iso2, int n, double* __restrict__ frames) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  pose_frame_one(eta + 7 * b, iso0, iso1, iso2, frames + 12 * b);
 }
 
 // dL/deta = J^T dL/dframe with J = d frame / d eta (12 x 7).
@@ -98,16 +102,19 @@ struct RegConfig {
 // come from k_image_loss on the current pose; gframes from drr_backward.
 // Trace rows are written at index `iter` (trace_eta n x (max_iters+1) x 6,
 // trace_loss n x (max_iters+1)); n_rec counts recorded rows.
-__global__ void k_register_update(double* __restrict__ eta, double* __restrict__ vel,
-                                  const double* __restrict__ gframes,
-                                  const double* __restrict__ value,
-                                  const int* __restrict__ loss_status, RegConfig cfg,
-                                  int iter, int* __restrict__ state, int* __restrict__ n_rec,
-                                  double* __restrict__ trace_eta,
-                                  double* __restrict__ trace_loss, int n) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= n) return;
-  if (state[b] != kRegRunning) return;
+// One iteration of registration b (registration.py:89-125): records the
+// trace row `iter`, sets the state on failure / convergence / the last
+// iteration, else applies the momentum step with the pose gradient of
+// dL/dframe `gf`.  Returns true when eta changed.
+__device__ __forceinline__ bool register_update_one(int b, double* __restrict__ eta,
+                                                    double* __restrict__ vel,
+                                                    const double* __restrict__ gf, double value,
+                                                    int loss_status, const RegConfig& cfg,
+                                                    int iter, int* __restrict__ state,
+                                                    int* __restrict__ n_rec,
+                                                    double* __restrict__ trace_eta,
+                                                    double* __restrict__ trace_loss) {
+  if (state[b] != kRegRunning) return false;
   double* e = eta + 7 * b;
   const int row = iter;
   double* te = trace_eta + (static_cast<int64_t>(b) * (cfg.max_iters + 1) + row) * 6;
@@ -121,17 +128,16 @@ __global__ void k_register_update(double* __restrict__ eta, double* __restrict__
 #pragma unroll
   for (int k = 0; k < 7; ++k) finite = finite && isfinite(e[k]);
   const bool gimbal = !(fabs(sin(e[2])) > 1e-6);
-  if (loss_status[b] != 0 || gimbal || !finite) {
+  if (loss_status != 0 || gimbal || !finite) {
     trace_loss[static_cast<int64_t>(b) * (cfg.max_iters + 1) + row] = INFINITY;
     state[b] = kRegFailed;
-    return;
+    return false;
   }
-  const double v = value[b];
-  trace_loss[static_cast<int64_t>(b) * (cfg.max_iters + 1) + row] = v;
-  if (v < cfg.threshold) { state[b] = kRegConverged; return; }
-  if (iter == cfg.max_iters) { state[b] = kRegDone; return; }
+  trace_loss[static_cast<int64_t>(b) * (cfg.max_iters + 1) + row] = value;
+  if (value < cfg.threshold) { state[b] = kRegConverged; return false; }
+  if (iter == cfg.max_iters) { state[b] = kRegDone; return false; }
   double g[7];
-  pose_grad(e, gframes + 12 * b, g);
+  pose_grad(e, gf, g);
   double* vb = vel + 6 * b;
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
@@ -139,6 +145,24 @@ __global__ void k_register_update(double* __restrict__ eta, double* __restrict__
     vb[k] = cfg.momentum * vb[k] - beta * g[1 + k];
     e[1 + k] += vb[k];
   }
+  return true;
+}
+
+// One iteration for each of n independent registrations.  `value`/`status`
+// come from k_image_loss on the current pose; gframes from drr_backward.
+// Trace rows are written at index `iter` (trace_eta n x (max_iters+1) x 6,
+// trace_loss n x (max_iters+1)); n_rec counts recorded rows.
+__global__ void k_register_update(double* __restrict__ eta, double* __restrict__ vel,
+                                  const double* __restrict__ gframes,
+                                  const double* __restrict__ value,
+                                  const int* __restrict__ loss_status, RegConfig cfg,
+                                  int iter, int* __restrict__ state, int* __restrict__ n_rec,
+                                  double* __restrict__ trace_eta,
+                                  double* __restrict__ trace_loss, int n) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  register_update_one(b, eta, vel, gframes + 12 * b, value[b], loss_status[b], cfg, iter, state,
+                      n_rec, trace_eta, trace_loss);
 }
 
 }  // namespace drr

@@ -199,3 +199,32 @@ def test_image_loss_cluster_edge_sizes(cuda_device):
             assert float(val[i]) == pytest.approx(rv, abs=1e-12)
             np.testing.assert_allclose(grad[i].cpu().numpy(), rg, rtol=1e-5,
                                        atol=1e-6 * np.abs(rg).max())
+
+
+def test_engine_three_launch_iteration_matches(golden, cuda_device):
+    """RegistrationEngine in the fused mode (drr_register_step: walk, loss,
+    reduction + update + next frames) against the stored-Jacobian mode: the
+    same convergence, losses within float32 pixel-gradient rounding, and the
+    graph-captured run equal to the eager one bit for bit."""
+    from paper_2208_12737_b200 import DeviceVolume, Detector
+    from paper_2208_12737_b200.registration import OptimizerConfig, RegistrationEngine
+    vol = DeviceVolume.from_flat(golden["ps_flat"], golden["ps_dims"], golden["ps_spacing"],
+                                 golden["ps_origin"], device=cuda_device)
+    det = Detector(21, 21, 4.0)
+    p0 = np.stack([golden["reg0_pose0"], golden["reg1_pose0"]])
+    cfg = OptimizerConfig(max_iters=40)
+    out = {}
+    for mode, graph in (("jac", True), ("fused", True), ("fused", False)):
+        eng = RegistrationEngine(vol, det, golden["ps_fixed"], 2, cfg, mode=mode)
+        eng.reset(p0)
+        eng.run(use_graph=graph)
+        out[(mode, graph)] = eng.traces()
+    for a, b in zip(out[("fused", True)], out[("fused", False)]):
+        np.testing.assert_array_equal(a.losses, b.losses)
+        np.testing.assert_array_equal(a.poses, b.poses)
+    for a, b in zip(out[("fused", True)], out[("jac", True)]):
+        assert a.converged == b.converged and a.failed == b.failed
+        n = min(len(a.losses), len(b.losses))
+        np.testing.assert_allclose(a.losses[:n], b.losses[:n], atol=1e-5)
+    for i, tr in enumerate(out[("fused", True)]):
+        assert tr.converged == bool(golden[f"reg{i}_converged"])
