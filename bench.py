@@ -353,7 +353,8 @@ def other_configs(sd, dev, timed, world, rank):
                                      "excluded; the reference's bar is rel < 1e-5",
                            **fd}
         out["C3"] = {"workload": "slice-to-volume registration on C2: 250 momentum-GD steps "
-                                 "(251 fwd+bwd iterations) of neg-ZNCC, whole loop one CUDA graph",
+                                 "(251 fwd+bwd iterations) of neg-ZNCC, whole loop one CUDA graph, "
+                                 "3 launches per iteration (drr_register_step)",
                      "ms_total": reg_ms, "ms_per_step": reg_ms / (cfg.max_iters + 1),
                      "final_neg_zncc": eng.traces()[0].final_loss}
     # C5: 512^3 @ 0.703125, 1024^2 @ 0.703125, 64 poses fwd+bwd (loss_and_gradient
@@ -633,6 +634,7 @@ def run_reference(args, world):
     kind, worker = cpu_setup(synthetic.chest_phantom(DIMS))
     procs = os.cpu_count() or 1
     poses = synthetic.sample_poses(TRUTH, synthetic.NARROW_HALF_WIDTHS, args.batch, seed=0)
+    one = [worker(poses[i])[0] for i in range(3)]  # 1 process on 1 core first
     pool = CpuPool(worker, procs)
     times = []
     k = 0
@@ -654,6 +656,8 @@ def run_reference(args, world):
         "config": {"workload": WORKLOAD, "global_batch": args.batch, "poses_per_step": procs,
                    "parallelism": f"{procs} host processes"},
         "cpu_baseline": {"value": value, "unit": "DRR/s", "cores": procs, "kind": kind,
+                         "one_core": {"value": 1.0 / float(np.median(one)), "unit": "DRR/s",
+                                      "cores": 1, "sample": "3 poses, one at a time"},
                          "sample": f"{procs} poses per step (one per process) cycling through "
                                    f"the GPU arm's {args.batch}-pose batch, fork pool created "
                                    f"once before warm-up; CPU {cpu_model()}"},
