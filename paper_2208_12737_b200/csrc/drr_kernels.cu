@@ -19,6 +19,7 @@
 //   k_count          used voxel-steps per ray (roofline denominator)
 // loss_kernels.cuh / pose_kernels.cuh hold the loss, pose-frame and
 // registration-update kernels of the batched loss_and_gradient chain.
+#include <cuda/atomic>
 #include <cuda_runtime.h>
 #include <limits.h>
 #include <math.h>
@@ -520,14 +521,19 @@ __global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
 #pragma unroll
       for (int k = 0; k < kFrameGrads; ++k) warp_part[warp][wsel * kFrameGrads + k] = v[k];
   }
+  // Arrival: a block-scope acq_rel RMW by the writing lane releases this
+  // warp's row and, for the last warp, acquires every other warp's (their RMWs
+  // form one release sequence on `arrivals`); __syncwarp then orders the row
+  // reads of all 32 lanes after it.  (compute-sanitizer racecheck models only
+  // barriers and reports this fence-free handshake as hazards.)
   int last = 0;
   if (lane == 0) {
-    __threadfence_block();  // this warp's row before its arrival
-    last = atomicAdd(&arrivals, 1) == kThreads / 32 - 1;
+    cuda::atomic_ref<int, cuda::thread_scope_block> count(arrivals);
+    last = count.fetch_add(1, cuda::memory_order_acq_rel) == kThreads / 32 - 1;
   }
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
-  __threadfence_block();  // every other warp's row after their arrivals
+  __syncwarp();
   const int blocks_per_pose = gridDim.x * gridDim.y;
   const CtaPos c = cta_pos(det);
   const int blk = c.ty * gridDim.x + c.tx;

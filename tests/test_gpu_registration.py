@@ -228,3 +228,33 @@ def test_engine_three_launch_iteration_matches(golden, cuda_device):
         np.testing.assert_allclose(a.losses[:n], b.losses[:n], atol=1e-5)
     for i, tr in enumerate(out[("fused", True)]):
         assert tr.converged == bool(golden[f"reg{i}_converged"])
+
+
+def test_c3_scale_register_vs_reference(cuda_device):
+    """C3 at full scale: api.register (float64, the device engine) against the
+    reference's own register (oracle/_ref, native backend) on the C2 chest
+    volume and 200^2 detector, for the first iterations (each reference
+    iteration is ~2 s of CPU): every loss to 1e-9, every pose to 1e-7."""
+    import math
+    from oracle.oracle import reference_module
+    from paper_2208_12737_b200 import api, synthetic
+    dt = reference_module()
+    if dt is None:
+        pytest.skip("oracle/_ref not built")
+    chest = synthetic.chest_phantom().astype(np.float64)
+    sp = (0.703125, 0.703125, 2.5)
+    truth = np.array([300.0, math.pi / 2, math.pi / 2, 0.0, 0.0, 0.0, 0.0])
+    pose0 = synthetic.sample_poses(truth, synthetic.NARROW_HALF_WIDTHS, 1, seed=0)[0]
+    rvol = dt.Volume((512, 512, 133), sp, (0.0, 0.0, 0.0), chest)
+    rspec = dt.DetectorSpec.for_volume(rvol, 200, 200, (3.6, 3.6))
+    fixed = dt.render(rvol, dt.PoseParameters.from_vector(truth), rspec)
+    cfg = dict(max_iters=2, converged_threshold=-1.1)
+    ref = dt.register(fixed, rvol, dt.PoseParameters.from_vector(pose0), rspec,
+                      dt.OptimizerConfig(**cfg))
+    vol = api.Volume((512, 512, 133), sp, (0.0, 0.0, 0.0), chest)
+    spec = api.DetectorSpec.for_volume(vol, 200, 200, (3.6, 3.6))
+    got = api.register(fixed, vol, api.PoseParameters.from_vector(pose0), spec,
+                       api.OptimizerConfig(**cfg))
+    assert len(got.losses) == len(ref.losses) == 3
+    np.testing.assert_allclose(got.losses, ref.losses, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(got.poses, ref.poses, rtol=0, atol=1e-7)
