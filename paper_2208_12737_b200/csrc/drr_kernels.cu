@@ -55,6 +55,11 @@ namespace drr {
 #ifndef DRR_SPLIT_MINB
 #define DRR_SPLIT_MINB 6
 #endif
+// the gradient walks with rays split over K > 1 lanes (a 4-deep gather
+// pipeline, DRR_LEAN_PIPE_GRAD_SPLIT): A/B one C2 pose, fwd+jac 0.119 -> 0.107 ms
+#ifndef DRR_SPLIT_MINB_GRAD
+#define DRR_SPLIT_MINB_GRAD 5
+#endif
 constexpr int kThreads = 128;  // 4 warps per CTA
 constexpr int kFrameGrads = 12;
 
@@ -191,7 +196,7 @@ __device__ __forceinline__ void store_out(OT* p, double v) {
 template <typename VT, int kMode, bool kChunked>
 __device__ __forceinline__ void walk_sums(const VT* __restrict__ vol, const GridDev& g,
                                           double* tab, const Ray& r, LeanSums& o) {
-  lean_walk<VT, kMode>(vol, g, tab, tab + plane_table_span(g), r, o);
+  lean_walk<VT, kMode, kChunked>(vol, g, tab, tab + plane_table_span(g), r, o);
 }
 
 // ---------------------------------------------------------------- forward
@@ -280,7 +285,7 @@ __device__ __forceinline__ void sums_to_endpoint_grads(const Ray& r, double acc,
 
 // --------------------------------------------------------------- backward
 template <typename VT, typename GT, typename OT, int K>
-__global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
+__global__ void __launch_bounds__(kThreads, K == 1 ? DRR_BWD_MINB : DRR_SPLIT_MINB_GRAD)
     k_backward(const VT* __restrict__ vol, const GridDev g,
                const double* __restrict__ frames, const DetDev det,
                const GT* __restrict__ grad_img, OT* __restrict__ img,
@@ -375,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, DRR_BWD_MINB)
 // derivatives are stored (SoA, jac[c * npix_total + pix], f64) and
 // k_backward_jac contracts them with it -- no second walk of the CT.
 template <typename VT, typename OT, int K>
-__global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
+__global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FJ_MINB : DRR_SPLIT_MINB_GRAD)
     k_forward_jac(const VT* __restrict__ vol, const GridDev g,
                   const double* __restrict__ frames, const DetDev det,
                   OT* __restrict__ img, double* __restrict__ jac, size_t npix_total) {
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
 // the step, and any batch size takes the one-walk path.
 constexpr int kLossSums = 3 * kFrameGrads;
 template <typename VT, typename OT, int K>
-__global__ void __launch_bounds__(kThreads, DRR_FJ_MINB)
+__global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FJ_MINB : DRR_SPLIT_MINB_GRAD)
     k_forward_loss(const VT* __restrict__ vol, const GridDev g,
                    const double* __restrict__ frames, const DetDev det,
                    OT* __restrict__ img, const OT* __restrict__ fixed, int64_t fixed_stride,

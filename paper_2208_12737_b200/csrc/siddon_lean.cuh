@@ -44,6 +44,11 @@ namespace drr {
 #ifndef DRR_LEAN_PIPE_GRAD
 #define DRR_LEAN_PIPE_GRAD 3
 #endif
+// rays split over K > 1 lanes (few-pose launches: one wave or less, so latency
+// matters more than occupancy) -- with 5 CTAs/SM (DRR_SPLIT_MINB_GRAD)
+#ifndef DRR_LEAN_PIPE_GRAD_SPLIT
+#define DRR_LEAN_PIPE_GRAD_SPLIT 4
+#endif
 #ifndef DRR_LEAN_Q_FWD
 #define DRR_LEAN_Q_FWD 0
 #endif
@@ -428,16 +433,17 @@ __device__ __forceinline__ void safe_walk(const VT* __restrict__ vol, const Grid
   }
 }
 
-template <typename VT, int kMode>
+template <typename VT, int kMode, bool kSplit = false>
 __device__ __forceinline__ void lean_walk(const VT* __restrict__ vol, const GridDev& g,
                                           const double* __restrict__ tab, double* rec,
                                           const Ray& r, LeanSums& o) {
+  constexpr int kPipeGrad = kSplit ? DRR_LEAN_PIPE_GRAD_SPLIT : DRR_LEAN_PIPE_GRAD;
   if (r.safe)
     safe_walk<VT, kMode>(vol, g, tab, r, o);
   else if (kMode == kLeanGrad && DRR_LEAN_DERIVE && r.lab_min != kConstLabel)
-    lean_walk_impl<VT, kMode, DRR_LEAN_PIPE_GRAD, DRR_LEAN_Q_GRAD, true>(vol, g, tab, rec, r, o);
+    lean_walk_impl<VT, kMode, kPipeGrad, DRR_LEAN_Q_GRAD, true>(vol, g, tab, rec, r, o);
   else
-    lean_walk_impl<VT, kMode, kMode == kLeanGrad ? DRR_LEAN_PIPE_GRAD : DRR_LEAN_PIPE_FWD,
+    lean_walk_impl<VT, kMode, kMode == kLeanGrad ? kPipeGrad : DRR_LEAN_PIPE_FWD,
                    kMode == kLeanGrad ? DRR_LEAN_Q_GRAD : DRR_LEAN_Q_FWD, false>(vol, g, tab, rec,
                                                                                  r, o);
 }

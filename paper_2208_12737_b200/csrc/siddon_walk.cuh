@@ -86,6 +86,14 @@ __device__ __forceinline__ double load_voxel(const VT* __restrict__ vol, int i) 
   return static_cast<double>(__ldg(vol + i));
 }
 
+// Setup divisions (entry / exit, first crossings, counts) by the walk's
+// Markstein form instead of IEEE '/' -- both correctly rounded, so the same
+// bits (all GPU parity tests); A/B (scripts/gpu_ab_var.sh, 256 C2 poses):
+// fwd+jac 10.35 -> 9.97 ms.
+#ifndef DRR_SETUP_DIVRN
+#define DRR_SETUP_DIVRN 1
+#endif
+
 // Correctly rounded num / d given inv = RN(1/d) (Markstein correction).
 __device__ __forceinline__ double div_rn(double num, double d, double inv) {
   const double q0 = __dmul_rn(num, inv);
@@ -207,8 +215,15 @@ __device__ __forceinline__ void entry_exit(const GridDev& g, Ray& r) {
       cmin[a] = inside ? -INFINITY : INFINITY;
       cmax[a] = inside ? INFINITY : -INFINITY;
     } else {
+#if DRR_SETUP_DIVRN
+      // correctly rounded like IEEE '/', by the walk's Markstein form (r.inv
+      // and r.safe are set before entry_exit in this build)
+      double a0 = r.safe ? (g.tlo[a] - r.s[a]) / r.d[a] : div_rn(g.tlo[a] - r.s[a], r.d[a], r.inv[a]);
+      double a1 = r.safe ? (g.thi[a] - r.s[a]) / r.d[a] : div_rn(g.thi[a] - r.s[a], r.d[a], r.inv[a]);
+#else
       double a0 = (g.tlo[a] - r.s[a]) / r.d[a];
       double a1 = (g.thi[a] - r.s[a]) / r.d[a];
+#endif
       if (a0 > a1) { const double t = a0; a0 = a1; a1 = t; }
       cmin[a] = a0;
       cmax[a] = a1;
@@ -256,11 +271,11 @@ __device__ __forceinline__ int first_plane_after(const GridDev& g, const Ray& r,
   for (int it = 0; it < 64; ++it) {
     const int kb = k - st;
     if (kb >= 0 && kb <= n) {
-      const double ab = plane_alpha(o, sp, kb, s, d, inv, true);
+      const double ab = plane_alpha(o, sp, kb, s, d, inv, !DRR_SETUP_DIVRN || r.safe);
       if (strict ? ab > a_s : ab >= a_s) { k = kb; continue; }
     }
     if (k >= 0 && k <= n) {
-      const double ak = plane_alpha(o, sp, k, s, d, inv, true);
+      const double ak = plane_alpha(o, sp, k, s, d, inv, !DRR_SETUP_DIVRN || r.safe);
       if (!(strict ? ak > a_s : ak >= a_s)) { k += st; continue; }
     }
     break;
@@ -272,7 +287,7 @@ __device__ __forceinline__ double axis_alpha(const GridDev& g, const Ray& r, int
   double o, sp, s, d, inv;
   int st, n;
   axis_params(g, r, a, o, sp, s, d, inv, st, n);
-  return plane_alpha(o, sp, k, s, d, inv, true);
+  return plane_alpha(o, sp, k, s, d, inv, !DRR_SETUP_DIVRN || r.safe);
 }
 
 // Trim [amin, amax] to the occupied hull (GridDev::hull), exactly.  fp32 slab
@@ -376,8 +391,18 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
     r.s[a] = s[a];
     r.d[a] = p[a] - s[a];
   }
-  entry_exit(g, r);
+#if DRR_SETUP_DIVRN
   r.safe = false;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    r.inv[a] = r.d[a] == 0.0 ? 0.0 : __drcp_rn(r.d[a]);
+    if (r.d[a] != 0.0 && !(fabs(r.d[a]) > 1e-20)) r.safe = true;
+  }
+#endif
+  entry_exit(g, r);
+#if !DRR_SETUP_DIVRN
+  r.safe = false;
+#endif
   r.end_lab = kNoEndLab;
   if (!r.hit) return;
   double T = 0.0, wmax = -1.0;
@@ -401,7 +426,11 @@ __device__ __forceinline__ void ray_setup(const GridDev& g, const double* s,
     // seg > 2^-39 * (M + 1) * sp / |d| guarantees floor(midpoint) equals the
     // next-plane bookkeeping with a 2^10 safety factor.
     const double M = fabs(r.s[a]) + fabs(d) + fabs(g.o[a]) + fabs(g.hi[a]) + g.sp[a];
+#if DRR_SETUP_DIVRN
+    T = fmax(T, 0x1.0p-39 * M * fabs(inv));  // a threshold: any rounding is fine (2^10 margin)
+#else
     T = fmax(T, 0x1.0p-39 * M / fabs(d));
+#endif
     const double w = fabs(d) / g.sp[a];
     if (w > wmax) { wmax = w; D = a; }
   }
