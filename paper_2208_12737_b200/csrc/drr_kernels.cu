@@ -19,7 +19,6 @@
 //   k_count          used voxel-steps per ray (roofline denominator)
 // loss_kernels.cuh / pose_kernels.cuh hold the loss, pose-frame and
 // registration-update kernels of the batched loss_and_gradient chain.
-#include <cuda/atomic>
 #include <cuda_runtime.h>
 #include <limits.h>
 #include <math.h>
@@ -451,8 +450,6 @@ __global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FJ_MINB : DRR_SPLIT_MIN
                    OT* __restrict__ img, const OT* __restrict__ fixed, int64_t fixed_stride,
                    double* __restrict__ partials) {
   extern __shared__ __align__(16) double tab[];
-  __shared__ int arrivals;  // warps done with the walk (the last one reduces)
-  if (threadIdx.x == 0) arrivals = 0;
   build_plane_table(g, frames + 12 * cta_pos(det).b, tab);  // s of this CTA's pose
   __syncthreads();
   int h, w, chunk;
@@ -504,12 +501,14 @@ __global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FJ_MINB : DRR_SPLIT_MIN
       }
     }
   }
-  // Fixed-order CTA sums of w * J for w = 1, a, b: xor butterfly in each warp
-  // (all 36 chains independent), then the 4 warps in index order -- summed by
-  // whichever warp finishes last (a shared-memory arrival count), so no warp
-  // waits at a CTA barrier for the slowest walk of its CTA (A/B: a barrier
-  // here made the kernel ~4% slower than k_forward_jac, whose warps exit as
-  // soon as their walks end).
+  // Fixed-order CTA sums of w * J for w = 1, a, b: an xor butterfly in each
+  // warp (all 36 chains independent), then the 4 warp rows in index order
+  // after one CTA barrier -- one 36-sum row per CTA, so the reduction kernel
+  // stays short for a single split pose.  A/B: the barrier costs ~0.6% at 256
+  // poses against warps writing their own rows (warp rows made the C3
+  // reduction 4x longer: +6 us per registration step), and a last-warp
+  // counter instead (correct under release/acquire) is invisible to
+  // compute-sanitizer's racecheck.
   __shared__ double warp_part[kThreads / 32][kLossSums];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
@@ -526,29 +525,15 @@ __global__ void __launch_bounds__(kThreads, K == 1 ? DRR_FJ_MINB : DRR_SPLIT_MIN
 #pragma unroll
       for (int k = 0; k < kFrameGrads; ++k) warp_part[warp][wsel * kFrameGrads + k] = v[k];
   }
-  // Arrival: a block-scope acq_rel RMW by the writing lane releases this
-  // warp's row and, for the last warp, acquires every other warp's (their RMWs
-  // form one release sequence on `arrivals`); __syncwarp then orders the row
-  // reads of all 32 lanes after it.  (compute-sanitizer racecheck models only
-  // barriers and reports this fence-free handshake as hazards.)
-  int last = 0;
-  if (lane == 0) {
-    cuda::atomic_ref<int, cuda::thread_scope_block> count(arrivals);
-    last = count.fetch_add(1, cuda::memory_order_acq_rel) == kThreads / 32 - 1;
-  }
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  __syncwarp();
-  const int blocks_per_pose = gridDim.x * gridDim.y;
-  const CtaPos c = cta_pos(det);
-  const int blk = c.ty * gridDim.x + c.tx;
-  double* out = partials + (static_cast<size_t>(c.b) * blocks_per_pose + blk) * kLossSums;
-  for (int t = lane; t < kLossSums; t += 32) {
-    const volatile double* col = &warp_part[0][t];
+  __syncthreads();
+  if (threadIdx.x < kLossSums) {
     double sacc = 0.0;
 #pragma unroll
-    for (int q = 0; q < kThreads / 32; ++q) sacc += col[q * kLossSums];
-    out[t] = sacc;
+    for (int q = 0; q < kThreads / 32; ++q) sacc += warp_part[q][threadIdx.x];
+    const int blocks_per_pose = gridDim.x * gridDim.y;
+    const CtaPos c = cta_pos(det);
+    const int blk = c.ty * gridDim.x + c.tx;
+    partials[(static_cast<size_t>(c.b) * blocks_per_pose + blk) * kLossSums + threadIdx.x] = sacc;
   }
 }
 
@@ -1214,9 +1199,9 @@ static int loss_step(const void* d_vol, int vol_dtype, const drr_grid* grid,
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int K = ray_split(d, n_poses);
   const dim3 grd = pose_grid(d, n_poses, K);
-  const int tiles = static_cast<int>(grd.x * grd.y);
+  const int rows = static_cast<int>(grd.x * grd.y);  // one 36-sum row per CTA
   double* partials = static_cast<double*>(d_workspace);
-  double* coef = partials + static_cast<size_t>(n_poses) * tiles * drr::kLossSums;
+  double* coef = partials + static_cast<size_t>(n_poses) * rows * drr::kLossSums;
   DRR_DISPATCH_K(K,
     if (vol_dtype == DRR_VOL_F32 && img_dtype == 0) {
       ensure_smem(drr::k_forward_loss<float, float, kK>, smem);
@@ -1259,7 +1244,7 @@ static int loss_step(const void* d_vol, int vol_dtype, const drr_grid* grid,
   }
   if (d_grad_frames == nullptr && d_grad_eta == nullptr && !reg.on) return DRR_OK;
   drr::k_reduce_loss_grad<<<n_poses, drr::kReduceLossThreads, 0, st>>>(
-      partials, tiles, coef, d_eta, d_grad_frames, d_grad_eta, reg);
+      partials, rows, coef, d_eta, d_grad_frames, d_grad_eta, reg);
   return check_launch("drr_forward_loss_grad/reduce");
 }
 
