@@ -451,9 +451,8 @@ def main():
     value = GB / (ms_per_step / 1e3)
     # native launches per step on each rank (registration._Buffers picks the chain)
     mode = next(b.mode for k, b in sd._bufs.items() if k[0] == "lg")
-    launches_per_step = 6 if mode == "jac" else 4
-    chain = ("jac: pose_frames, forward_jac, image_loss, backward_jac, reduce_frames, pose_grad"
-             if mode == "jac" else
+    launches_per_step = 3 if mode == "jac" else 4
+    chain = ("jac: pose_frames, forward_jac, loss_grad_jac" if mode == "jac" else
              "fused: pose_frames, forward_loss, image_loss, reduce_loss_grad")
 
     # --- e2e: public API, pinned host poses in, loss + grads back out ------
@@ -503,8 +502,19 @@ def main():
 
     def k_fj():
         hold["img"], hold["jac"] = render_frames_jac(sd.volume, sd.detector, frames)
+
+    from paper_2208_12737_b200 import _lib as L
+    lg_val = torch.empty(B, dtype=torch.float64, device=dev)
+    lg_gf = torch.empty((B, 12), dtype=torch.float64, device=dev)
+
+    def lgj(h):  # the step's tail: loss + pixel gradient + contraction (one launch)
+        L.check(L.load().drr_loss_grad_jac(
+            h["jac"].data_ptr(), h["img"].data_ptr(), fixed.data_ptr(), 0, 0, B,
+            sd.detector.c, L.DRR_LOSS_NEG_ZNCC, lg_val.data_ptr(), None,
+            lg_gf.data_ptr(), None, None, torch.cuda.current_stream(dev).cuda_stream))
     kfns = {"fj": k_fj,
             "bj": lambda: backward_from_jac(sd.detector, hold["jac"], g_img),
+            "lgj": lambda: lgj(hold),
             "fwd": lambda: render_frames(sd.volume, sd.detector, frames),
             "rewalk": lambda: backward_frames(sd.volume, sd.detector, frames, g_img)}
     kt = {k: [] for k in kfns}
@@ -605,6 +615,7 @@ def main():
                      "limiter": ncu.get("limiter"), "limiter_frac": ncu.get("limiter_frac"),
                      "traffic_source": ncu.get("capture")},
         "kernels": {"forward_jac_ms": kms["fj"], "backward_jac_ms": kms["bj"],
+                    "loss_grad_jac_ms": kms["lgj"],
                     "forward_only_ms": kms["fwd"], "rewalk_backward_ms": kms["rewalk"],
                     "voxel_steps_per_drr": S / B,
                     "walked_voxel_steps_per_drr": S_walk / B,

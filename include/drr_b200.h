@@ -37,6 +37,8 @@
  *                               -> dL/d(rho, theta, phi, gamma, bx, by, bz)
  *   drr_image_loss           <- metrics.py:71-91 loss_value_and_pixel_grad
  *                               (neg_zncc, l2), batched, fused
+ *   drr_loss_grad_jac        <- gradients.py:61-69's loss, pixel gradient and
+ *                               pixel_grad @ d_image from stored Jacobians
  *   drr_forward_loss_grad    <- gradients.py:61-69 loss_and_gradient for the
  *                               two losses of metrics.py:71-91, batched: one
  *                               walk per ray, no stored Jacobian
@@ -260,6 +262,19 @@ int drr_forward_loss_grad(const void *d_vol, int vol_dtype, const drr_grid *grid
                           int *d_status, double *d_grad_frames,
                           double *d_grad_eta, void *d_workspace,
                           size_t workspace_bytes, void *stream);
+
+/* The stored-Jacobian step's tail in one launch: per image (one 8-CTA
+ * cluster) the neg-ZNCC / L2 value and status (as drr_image_loss), then the
+ * float64 pixel gradient contracted with drr_forward_jac's d_jac (6 x
+ * (B*H*W)) into d_grad_frames (B x 12, may be NULL) and, given d_eta,
+ * d_grad_eta (B x 7) -- in place of drr_image_loss + drr_backward_jac +
+ * drr_pose_grad.  img_dtype 0 / 1 as drr_forward_jac's image (d_fixed the
+ * same dtype); fixed_stride 0 or H*W; n_images <= 65535. */
+int drr_loss_grad_jac(const double *d_jac, const void *d_img, const void *d_fixed,
+                      int img_dtype, int64_t fixed_stride, int32_t n_images,
+                      const drr_detector *det, int kind, double *d_value,
+                      int *d_status, double *d_grad_frames, const double *d_eta,
+                      double *d_grad_eta, void *stream);
 
 /* Momentum gradient descent settings (registration.py:41-58). */
 typedef struct drr_reg_config {

@@ -47,6 +47,7 @@ EXPORTS = (
     "drr_image_loss",
     "drr_register_update",
     "drr_register_step",
+    "drr_loss_grad_jac",
     "drr_loss_grad_workspace_size",
     "drr_forward_loss_grad",
     "drr_peer_export",
@@ -118,6 +119,8 @@ _SIGNATURES = {
     "drr_register_update": ([_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(DrrRegConfig), _i32,
                              _vp, _vp, _vp, _vp, _i32, _vp], _int),
     "drr_loss_grad_workspace_size": ([_i32, _DP], _sz),
+    "drr_loss_grad_jac": ([_vp, _vp, _vp, _int, _i64, _i32, _DP, _int, _vp, _vp, _vp, _vp, _vp,
+                           _vp], _int),
     "drr_forward_loss_grad": ([_vp, _int, _GP, _vp, _vp, _i32, _DP, _vp, _i64, _int, _vp, _int,
                                _vp, _vp, _vp, _vp, _vp, _sz, _vp], _int),
     "drr_register_step": ([_vp, _int, _GP, _vp, _vp, _vp, _i32, _DP, _vp, _i64, _int, _vp, _int,

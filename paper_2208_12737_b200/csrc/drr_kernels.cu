@@ -820,6 +820,158 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ------------------------------------------- loss + Jacobian contraction
+// The stored-Jacobian step's tail in ONE kernel per image (one 8-CTA
+// thread-block cluster, as k_image_loss): the two-pass neg-ZNCC / L2 moments
+// give the value and the pixel gradient's affine coefficients (c0, c1, c2)
+// on every thread; a third pass over the CTA's pixels contracts
+// g_i = c0 + c1 a_i + c2 b_i (float64, never stored) with the ray's stored
+// endpoint derivatives into the 12 frame sums, reduced in a fixed order
+// (warp butterflies, warps, then the cluster's CTAs in rank order through
+// distributed shared memory); rank 0 writes dL/dframe and, given eta,
+// chains it to dL/deta.  Replaces k_image_loss + k_backward_jac +
+// k_reduce_frames + k_pose_grad (four launches, and the fp32 pixel-gradient
+// round trip) for gradients.py:61-69 with the losses of metrics.py:71-91.
+template <typename IT>
+__global__ void __cluster_dims__(kLossCluster, 1, 1) __launch_bounds__(kLossThreads)
+    k_loss_grad_jac(const double* __restrict__ jac, size_t npix_total, const IT* __restrict__ img,
+                    const IT* __restrict__ fixed, int64_t fixed_stride, const DetDev det,
+                    int kind, double* __restrict__ value, int* __restrict__ status,
+                    double* __restrict__ grad_frames, const double* __restrict__ eta,
+                    double* __restrict__ grad_eta) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ double sm[(kLossThreads / 32 + 2) * 5];
+  __shared__ double wrow[kLossThreads / 32][kFrameGrads];
+  __shared__ double ctot[kFrameGrads];
+  const int b = blockIdx.y;
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int64_t npix = static_cast<int64_t>(det.H) * det.W;
+  const int64_t chunk = (npix + kLossCluster - 1) / kLossCluster;
+  const int64_t lo = rank * chunk, hi = lo + chunk < npix ? lo + chunk : npix;
+  const IT* a = img + static_cast<int64_t>(b) * npix;
+  const IT* f = fixed + static_cast<int64_t>(b) * fixed_stride;
+  const double N = static_cast<double>(npix);
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+  {
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kLossThreads) {
+      const double x = static_cast<double>(a[i]), y = static_cast<double>(f[i]);
+      if (kind == 0) {
+        v[0] += x; v[2] += y;
+      } else {
+        const double dd = x - y;
+        v[0] += dd * dd;
+      }
+    }
+    cluster_sum5<kLossThreads>(v, sm);
+    if (kind == 0) {
+      const double ma = v[0] / N, mb = v[2] / N;
+      const double a0 = static_cast<double>(a[0]), b0 = static_cast<double>(f[0]);
+      double w[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int64_t i = lo + threadIdx.x; i < hi; i += kLossThreads) {
+        const double x = static_cast<double>(a[i]), y = static_cast<double>(f[i]);
+        const double dx = x - ma, dy = y - mb;
+        w[0] += dx * dx; w[1] += dy * dy; w[2] += dx * dy;
+        w[3] += x != a0 ? 1.0 : 0.0;
+        w[4] += y != b0 ? 1.0 : 0.0;
+      }
+      cluster_sum5<kLossThreads>(w, sm);
+      const double sa = sqrt(w[0] / N), sb = sqrt(w[1] / N);
+      const bool undefined = w[3] == 0.0 || w[4] == 0.0 || !(sa > 0.0) || !(sb > 0.0);
+      const double raw = undefined ? NAN : w[2] / (N * sa * sb);
+      const double scale = undefined ? NAN : -1.0 / (N * sa);
+      c0 = scale * (raw * ma / sa - mb / sb);
+      c1 = -scale * raw / sa;
+      c2 = scale / sb;
+      if (rank == 0 && threadIdx.x == 0) {
+        value[b] = undefined ? NAN : -fmin(1.0, fmax(-1.0, raw));
+        if (status) status[b] = undefined ? 1 : 0;
+      }
+    } else {
+      const double norm = sqrt(v[0]);
+      const double inv = norm > 0.0 ? 1.0 / norm : 0.0;
+      c1 = inv;
+      c2 = -inv;
+      if (rank == 0 && threadIdx.x == 0) {
+        value[b] = norm;
+        if (status) status[b] = 0;
+      }
+    }
+  }
+  // contraction of this CTA's pixels (a missed ray's zero Jacobian adds nothing)
+  double acc[kFrameGrads];
+#pragma unroll
+  for (int k = 0; k < kFrameGrads; ++k) acc[k] = 0.0;
+  const size_t pbase = static_cast<size_t>(b) * npix;
+  // kLossBatch pixels' loads in flight before any is accumulated (in order)
+  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += kLossThreads * kLossBatch) {
+    double js[kLossBatch][3], jp[kLossBatch][3], xa[kLossBatch], yb[kLossBatch];
+#pragma unroll
+    for (int u = 0; u < kLossBatch; ++u) {
+      const int64_t i = i0 + static_cast<int64_t>(u) * kLossThreads;
+      const bool in = i < hi;
+      const size_t pix = pbase + (in ? i : lo);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        js[u][q] = in ? __ldg(jac + q * npix_total + pix) : 0.0;
+        jp[u][q] = in ? __ldg(jac + (3 + q) * npix_total + pix) : 0.0;
+      }
+      xa[u] = in ? static_cast<double>(a[i]) : 0.0;
+      yb[u] = in ? static_cast<double>(f[i]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kLossBatch; ++u) {
+      const int64_t i = i0 + static_cast<int64_t>(u) * kLossThreads;
+      if (i >= hi) break;
+      const double g = (c0 + c1 * xa[u]) + c2 * yb[u];
+      const int h = static_cast<int>(i / det.W), w = static_cast<int>(i % det.W);
+      const double ah = (static_cast<double>(h) - det.half_h) * det.pitch_y;
+      const double aw = (static_cast<double>(w) - det.half_w) * det.pitch_x;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        acc[q] += g * js[u][q];
+        acc[3 + q] += g * jp[u][q];
+        acc[6 + q] += g * ah * jp[u][q];
+        acc[9 + q] += g * aw * jp[u][q];
+      }
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int k = 0; k < kFrameGrads; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < kFrameGrads; ++k) wrow[warp][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < kFrameGrads) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kLossThreads / 32; ++q) t += wrow[q][threadIdx.x];
+    ctot[threadIdx.x] = t;
+  }
+  cluster.sync();  // every CTA's 12 totals are visible cluster-wide
+  if (rank == 0) {
+    __shared__ double gf[kFrameGrads];
+    if (threadIdx.x < kFrameGrads) {
+      double t = 0.0;
+      for (int r = 0; r < kLossCluster; ++r) t += *cluster.map_shared_rank(ctot + threadIdx.x, r);
+      gf[threadIdx.x] = t;
+      if (grad_frames) grad_frames[b * kFrameGrads + threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && grad_eta != nullptr) {
+      double ge[7];
+      pose_grad(eta + 7 * b, gf, ge);
+#pragma unroll
+      for (int q = 0; q < 7; ++q) grad_eta[7 * b + q] = ge[q];
+    }
+  }
+  cluster.sync();  // no CTA leaves while rank 0 reads its totals
+}
+
 // One CTA per pose: each thread sums a fixed strided subset of the CTA
 // partials, then a fixed shared-memory tree.
 constexpr int kReduceThreads = 128;
@@ -1651,6 +1803,41 @@ int drr_volume_pack(const void* d_src, int src_type, int src_order, const int64_
   else
     return fail(DRR_ERR_INVALID_ARGUMENT, "unknown dst_dtype %d", dst_dtype);
   return check_launch("drr_volume_pack");
+}
+
+int drr_loss_grad_jac(const double* d_jac, const void* d_img, const void* d_fixed, int img_dtype,
+                      int64_t fixed_stride, int32_t n_images, const drr_detector* det, int kind,
+                      double* d_value, int* d_status, double* d_grad_frames, const double* d_eta,
+                      double* d_grad_eta, void* stream) {
+  drr::DetDev d;
+  int rc = make_det(det, d);
+  if (rc) return rc;
+  if (n_images < 0 || n_images > 65535)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "n_images must be in [0, 65535], got %d", n_images);
+  if (n_images == 0) return DRR_OK;
+  if (kind != DRR_LOSS_NEG_ZNCC && kind != DRR_LOSS_L2)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "loss kind must be neg_zncc (0) or l2 (1), got %d", kind);
+  const int64_t npix = static_cast<int64_t>(d.H) * d.W;
+  if (fixed_stride != 0 && fixed_stride != npix)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "fixed_stride must be 0 or H*W");
+  if (d_jac == nullptr || d_img == nullptr || d_fixed == nullptr || d_value == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "d_jac, d_img, d_fixed and d_value must not be NULL");
+  if (d_grad_eta != nullptr && d_eta == nullptr)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "d_grad_eta needs d_eta");
+  if (img_dtype != 0 && img_dtype != 1)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown img_dtype %d", img_dtype);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const dim3 grd(drr::kLossCluster, n_images);
+  const size_t npix_total = static_cast<size_t>(n_images) * npix;
+  if (img_dtype == 0)
+    drr::k_loss_grad_jac<float><<<grd, drr::kLossThreads, 0, st>>>(
+        d_jac, npix_total, static_cast<const float*>(d_img), static_cast<const float*>(d_fixed),
+        fixed_stride, d, kind, d_value, d_status, d_grad_frames, d_eta, d_grad_eta);
+  else
+    drr::k_loss_grad_jac<double><<<grd, drr::kLossThreads, 0, st>>>(
+        d_jac, npix_total, static_cast<const double*>(d_img), static_cast<const double*>(d_fixed),
+        fixed_stride, d, kind, d_value, d_status, d_grad_frames, d_eta, d_grad_eta);
+  return check_launch("drr_loss_grad_jac");
 }
 
 int drr_count_steps(const void* d_vol, int vol_dtype, const drr_grid* grid,

@@ -6,9 +6,9 @@ and ``registration.register`` (``registration.py:89-125``), batched:
 * :func:`loss_and_gradient` -- B poses at once: ``drr_pose_frames`` -> one
   walk per ray -> the fused neg-ZNCC / L2 value and pixel gradient -> dL/dframe
   -> dL/deta, as native launches only (no host round trip, no torch
-  autograd).  Two chains (:class:`_Buffers`): the stored ray Jacobian and its
-  contraction (``drr_forward_jac`` / ``drr_image_loss`` /
-  ``drr_backward_jac``), or ``drr_forward_loss_grad`` (no Jacobian: per-CTA
+  autograd).  Two chains (:class:`_Buffers`): the stored ray Jacobian and
+  ``drr_loss_grad_jac`` (loss + pixel gradient + contraction + pose gradient
+  in one launch), or ``drr_forward_loss_grad`` (no Jacobian: per-CTA
   sums of the ray Jacobian weighted by 1, the image and the fixed image,
   combined with the loss kernel's affine pixel-gradient coefficients).
 * :class:`RegistrationEngine` -- B independent momentum-GD registrations
@@ -109,10 +109,10 @@ class _Buffers:
     Two native chains compute the same step (``mode``):
 
     * ``"jac"`` -- ``drr_forward_jac`` stores each ray's 6-double Jacobian
-      (48 B/pixel), ``drr_image_loss`` writes the pixel gradient and
-      ``drr_backward_jac`` contracts the two: measured ~3% faster at C2 (the
-      fused walk's per-CTA 36-sum epilogue costs more than the stored
-      contraction; profiles/r02/SUMMARY.md);
+      (48 B/pixel) and ``drr_loss_grad_jac`` computes the loss, its float64
+      pixel gradient and their contraction (and the pose gradient) in one
+      cluster launch per image: measured faster at C2 (the fused walk's
+      per-CTA 36-sum epilogue costs more; profiles/r02/SUMMARY.md);
     * ``"fused"`` -- ``drr_forward_loss_grad``: no Jacobian, the pixel gradient
       as an affine map of the two images reduced inside the walk; float64
       pixel gradients (used for float64 images) and any batch size.
@@ -145,9 +145,7 @@ class _Buffers:
         lib = _lib.load()
         if mode == "jac":
             self.jac = torch.empty((6, B * det.height * det.width), dtype=torch.float64, device=dev)
-            self.pix_grad = torch.empty((B, det.height, det.width), dtype=torch.float32,
-                                        device=dev)
-            self.ws_bytes = lib.drr_backward_workspace_size(B, det.c)
+            self.ws_bytes = 0
         else:
             self.ws_bytes = lib.drr_loss_grad_workspace_size(B, det.c)
         self.ws = torch.empty(max(self.ws_bytes, 8), dtype=torch.uint8, device=dev)
@@ -158,7 +156,8 @@ def _launch_loss_grad(lib, vol, det, iso, eta, fixed, fixed_stride, kind, buf, s
     """pose frames -> one walk per ray -> loss value + pixel gradient -> dL/dframe
     (buf.grad_frames) -> dL/deta (``grad_eta_ptr``, when given); the loss values
     go to ``value_ptr`` (or buf.value).  The output pointers may be another
-    rank's buffers (distributed.PeerRows).  ``buf.mode`` picks the chain."""
+    rank's buffers (distributed.PeerRows).  ``buf.mode`` picks the chain:
+    three launches either way."""
     B = buf.B
     value_ptr = buf.value.data_ptr() if value_ptr is None else value_ptr
     _lib.check(lib.drr_pose_frames(eta.data_ptr(), B, iso, buf.frames.data_ptr(), stream))
@@ -172,15 +171,12 @@ def _launch_loss_grad(lib, vol, det, iso, eta, fixed, fixed_stride, kind, buf, s
     _lib.check(lib.drr_forward_jac(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
                                    buf.frames.data_ptr(), B, det.c, buf.img.data_ptr(), 0,
                                    buf.jac.data_ptr(), stream))
-    _lib.check(lib.drr_image_loss(buf.img.data_ptr(), fixed.data_ptr(), 0, fixed_stride, B,
-                                  det.height * det.width, kind, value_ptr,
-                                  buf.pix_grad.data_ptr(), buf.status.data_ptr(), stream))
-    _lib.check(lib.drr_backward_jac(buf.jac.data_ptr(), B, det.c, buf.pix_grad.data_ptr(), 0,
-                                    buf.grad_frames.data_ptr(), buf.ws.data_ptr(),
-                                    buf.ws_bytes, stream))
-    if grad_eta_ptr is not None:
-        _lib.check(lib.drr_pose_grad(eta.data_ptr(), buf.grad_frames.data_ptr(), B,
-                                     grad_eta_ptr, stream))
+    # loss + float64 pixel gradient + contraction (+ pose gradient): one launch
+    _lib.check(lib.drr_loss_grad_jac(buf.jac.data_ptr(), buf.img.data_ptr(), fixed.data_ptr(), 0,
+                                     fixed_stride, B, det.c, kind, value_ptr,
+                                     buf.status.data_ptr(),
+                                     buf.grad_frames.data_ptr() if grad_frames else None,
+                                     eta.data_ptr(), grad_eta_ptr, stream))
 
 
 def _prep_fixed(fixed, B, det, dev, dtype=torch.float32):

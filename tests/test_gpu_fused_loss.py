@@ -233,3 +233,45 @@ def test_loss_and_gradient_chains_agree(cuda_device):
     torch.testing.assert_close(vj, vf, rtol=0, atol=0)
     scale = gf.abs().max(dim=1, keepdim=True).values
     assert bool(((gj - gf).abs() <= 1e-5 * scale).all()), (gj, gf)
+
+
+@pytest.mark.parametrize("kind", ["neg_zncc", "l2"])
+def test_loss_grad_jac_vs_oracle(cuda_device, kind):
+    """drr_loss_grad_jac (loss + float64 pixel gradient + Jacobian contraction
+    + pose gradient, one cluster launch per image) after drr_forward_jac:
+    values to 1e-12, dL/dframe and dL/deta to 1e-9 of the oracle, per-pose
+    fixed images and a shared one."""
+    from paper_2208_12737_b200 import Detector, DeviceVolume, _lib, pose_frames, render_frames_jac
+    v = _volume()
+    vol = DeviceVolume(v, SP, device=cuda_device, dtype=torch.float64)
+    det = Detector(H, W, 2.5, 2.25, ray_split=1)
+    eta = _poses(4, seed=17)
+    et = torch.tensor(eta, device=cuda_device)
+    fr = pose_frames(et, vol.center).detach()
+    img, jac = render_frames_jac(vol, det, fr, out_dtype=torch.float64)
+    flat = v.ravel(order="F")
+    rng = np.random.default_rng(9)
+    code = _lib.DRR_LOSS_NEG_ZNCC if kind == "neg_zncc" else _lib.DRR_LOSS_L2
+    for fixed, stride in ((rng.random((H, W)) * 30.0, 0), (rng.random((4, H, W)) * 30.0, H * W)):
+        fx = torch.tensor(fixed, device=cuda_device)
+        val = torch.empty(4, dtype=torch.float64, device=cuda_device)
+        gf = torch.empty((4, 12), dtype=torch.float64, device=cuda_device)
+        ge = torch.empty((4, 7), dtype=torch.float64, device=cuda_device)
+        st = torch.zeros(4, dtype=torch.int32, device=cuda_device)
+        _lib.check(_lib.load().drr_loss_grad_jac(
+            jac.data_ptr(), img.data_ptr(), fx.data_ptr(), 1, stride, 4, det.c, code,
+            val.data_ptr(), st.data_ptr(), gf.data_ptr(), et.data_ptr(), ge.data_ptr(),
+            torch.cuda.current_stream().cuda_stream))
+        for i in range(4):
+            fi = fixed if stride == 0 else fixed[i]
+            ref_img = O.render(flat, DIMS, SP, (0, 0, 0), fr[i].cpu().numpy(), H, W, 2.5, 2.25)
+            rv, pg = (O.neg_zncc_value_and_grad(ref_img, fi) if kind == "neg_zncc"
+                      else _l2_value_and_grad(ref_img, fi))
+            assert float(val[i]) == pytest.approx(rv, abs=1e-12, rel=1e-12)
+            _, rgf = O.render_backward(flat, DIMS, SP, (0, 0, 0), fr[i].cpu().numpy(), H, W, 2.5,
+                                       2.25, pg)
+            np.testing.assert_allclose(gf[i].cpu().numpy(), rgf, rtol=0,
+                                       atol=1e-9 * np.abs(rgf).max())
+            rge = rgf @ O.frame_jacobian(eta[i], vol.center)
+            np.testing.assert_allclose(ge[i].cpu().numpy(), rge, rtol=0,
+                                       atol=1e-9 * np.abs(rge).max())
