@@ -261,17 +261,25 @@ __global__ void __launch_bounds__(kThreads)
 
 // Endpoint gradients from summed walk totals (acc, G, H): the same algebra as
 // endpoint_grads, for chunked walks whose partial sums were combined.
+// Correctly rounded x / y -- the Markstein form (the walk's) when y is in the
+// normal range, else IEEE '/': the same bits either way, fewer instructions.
+__device__ __forceinline__ double cr_div(double x, double y, double rcp) {
+  return fabs(y) > 1e-20 ? div_rn(x, y, rcp) : x / y;
+}
+
 __device__ __forceinline__ void sums_to_endpoint_grads(const double* d, double acc,
                                                        const double* G, const double* Hh,
                                                        double L, double* dEds, double* dEdp) {
+  const double rL = __drcp_rn(L);
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double gs = 0.0, gp = 0.0;
     if (d[a] != 0.0) {
-      gs = L * (Hh[a] - G[a]) / d[a];
-      gp = -L * Hh[a] / d[a];
+      const double rd = __drcp_rn(d[a]);
+      gs = cr_div(L * (Hh[a] - G[a]), d[a], rd);
+      gp = cr_div(-L * Hh[a], d[a], rd);
     }
-    const double lt = d[a] / L * acc;
+    const double lt = cr_div(d[a], L, rL) * acc;
     dEds[a] = gs - lt;
     dEdp[a] = gp + lt;
   }
@@ -1145,6 +1153,7 @@ int make_grid(const drr_grid* in, drr::GridDev& g) {
     g.tlo[a] = in->origin[a] + plo;
     g.thi[a] = in->origin[a] + phi;
     g.isp[a] = static_cast<float>(1.0 / in->spacing[a]);
+    g.ispd[a] = 1.0 / in->spacing[a];
   }
   // the occupied hull (drr_volume_hull): n . (i, j, k) ranges of the non-zero
   // voxels -> the supports of their boxes [i, i+1] x ..., widened by 1/16 voxel
