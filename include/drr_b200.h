@@ -123,6 +123,10 @@ typedef struct drr_detector {
 
 const char *drr_last_error(void);
 int drr_version(void);
+/* sizeof the ABI structs as this library was compiled (a binding checks its
+ * own layouts against them; any pointer may be NULL). */
+int drr_struct_sizes(size_t *grid, size_t *detector, size_t *reg_config,
+                     size_t *peer_handle);
 
 /* Energies of explicit rays from one source: out[r] = |p_r - s| sum seg V.
  * d_src: 3 doubles, d_pix: N x 3 doubles, d_out: N doubles. */

@@ -29,6 +29,7 @@ DRR_VOL_F64 = 1
 EXPORTS = (
     "drr_last_error",
     "drr_version",
+    "drr_struct_sizes",
     "drr_raysum",
     "drr_raysum_endpoint_grad",
     "drr_forward",
@@ -100,6 +101,7 @@ _DP = ctypes.POINTER(DrrDetector)
 _SIGNATURES = {
     "drr_last_error": ([], ctypes.c_char_p),
     "drr_version": ([], _int),
+    "drr_struct_sizes": ([_vp, _vp, _vp, _vp], _int),
     "drr_raysum": ([_vp, _int, _GP, _vp, _vp, _i64, _vp, _vp], _int),
     "drr_raysum_endpoint_grad": ([_vp, _int, _GP, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _int),
     "drr_forward": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp], _int),
@@ -156,8 +158,20 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
+    _check_layouts(lib)
     _lib = lib
     return lib
+
+
+def _check_layouts(lib) -> None:
+    """The ctypes mirrors must have the library's struct sizes (a stale
+    library or binding would otherwise pass misaligned arguments)."""
+    got = [ctypes.c_size_t() for _ in range(4)]
+    lib.drr_struct_sizes(*[ctypes.byref(g) for g in got])
+    want = [ctypes.sizeof(t) for t in (DrrGrid, DrrDetector, DrrRegConfig, DrrPeerHandle)]
+    if [g.value for g in got] != want:
+        raise ImportError(f"{LIB_PATH}: ABI struct sizes {[g.value for g in got]} differ from "
+                          f"the ctypes layouts {want}; rebuild the library")
 
 
 def check(rc: int) -> None:

@@ -1414,7 +1414,15 @@ extern "C" {
 
 const char* drr_last_error(void) { return g_err; }
 
-int drr_version(void) { return 1; }
+int drr_version(void) { return 2; }
+
+int drr_struct_sizes(size_t* grid, size_t* detector, size_t* reg_config, size_t* peer_handle) {
+  if (grid) *grid = sizeof(drr_grid);
+  if (detector) *detector = sizeof(drr_detector);
+  if (reg_config) *reg_config = sizeof(drr_reg_config);
+  if (peer_handle) *peer_handle = sizeof(drr_peer_handle);
+  return DRR_OK;
+}
 
 int drr_raysum(const void* d_vol, int vol_dtype, const drr_grid* grid,
                const double* d_src, const double* d_pix, int64_t n_rays,

@@ -25,7 +25,13 @@ def test_exports_every_declared_symbol():
     assert set(declared) == set(_lib.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.drr_version() >= 1
+    assert lib.drr_version() >= 2
+    # the ctypes mirrors have the library's struct layouts (checked on load too)
+    import ctypes
+    got = [ctypes.c_size_t() for _ in range(4)]
+    assert lib.drr_struct_sizes(*[ctypes.byref(g) for g in got]) == 0
+    assert [g.value for g in got] == [ctypes.sizeof(t) for t in (
+        _lib.DrrGrid, _lib.DrrDetector, _lib.DrrRegConfig, _lib.DrrPeerHandle)]
 
 
 def test_library_is_sm100a():
