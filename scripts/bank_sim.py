@@ -9,7 +9,8 @@ loaded of 16 eight-byte bank slots.  Measurement script, CPU only.
 Result at C2 (4 narrow poses x 6 quads; ncu: 3.7 wavefronts per warp step):
 current concatenated tables 3.74, per-axis padding 3.72, axes interleaved with
 stride 4 4.51, slot groups (dominant axis 8 even slots, others 4 + 4) 3.67,
-plus warp-aligned starts 3.59; with 4x8 quads (/tmp-style diag) 3.32.
+plus warp-aligned starts 3.59; 4-wide x 8-high quads (`--quad 4x8`, current
+tables) 3.32.
 """
 import math
 import os
@@ -128,7 +129,7 @@ def wavefronts(reads_by_lane, fn):
     return tot, steps
 
 
-def main(n_poses=4, quads=6):
+def main(n_poses=4, quads=6, qw=8):
     rng = np.random.default_rng(0)
     poses = synthetic.sample_poses((300, math.pi / 2, math.pi / 2, 0, 0, 0, 0),
                                    synthetic.NARROW_HALF_WIDTHS, n_poses, seed=0)
@@ -143,7 +144,7 @@ def main(n_poses=4, quads=6):
             h0, w0 = rng.integers(40, 156), rng.integers(40, 150)
             lanes = []
             for lane in range(32):
-                h, w = h0 + lane // 8, w0 + lane % 8
+                h, w = h0 + lane // qw, w0 + lane % qw
                 lanes.append(p0 + (h - 99.5) * eh + (w - 99.5) * ew)
             for tag, al in (("", None), ("+align", D)):
                 reads = walk_reads(src, np.array(lanes), al)
@@ -159,4 +160,7 @@ def main(n_poses=4, quads=6):
 
 
 if __name__ == "__main__":
-    main()
+    qw = 8
+    if "--quad" in sys.argv:
+        qw = int(sys.argv[sys.argv.index("--quad") + 1].split("x")[0])
+    main(qw=qw)
