@@ -10,7 +10,7 @@ Result at C2 (4 narrow poses x 6 quads; ncu: 3.7 wavefronts per warp step):
 current concatenated tables 3.74, per-axis padding 3.72, axes interleaved with
 stride 4 4.51, slot groups (dominant axis 8 even slots, others 4 + 4) 3.67,
 plus warp-aligned starts 3.59; 4-wide x 8-high quads (`--quad 4x8`, current
-tables) 3.32.
+tables) 3.41.
 """
 import math
 import os
