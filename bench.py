@@ -546,12 +546,22 @@ def main():
             ncu = {"traffic": float(tr["traffic_bytes_per_launch"]) * per_pose * B,
                    "lts_bytes": (float(tr["lts_bytes_per_launch"]) * per_pose * B
                                  if "lts_bytes_per_launch" in tr else None),
+                   "gather_sector_bytes": (float(tr["gather_sector_bytes_per_launch"]) * per_pose * B
+                                           if "gather_sector_bytes_per_launch" in tr else None),
+                   "l2_to_sm_bytes": (float(tr["l2_to_sm_bytes_per_launch"]) * per_pose * B
+                                      if "l2_to_sm_bytes_per_launch" in tr else None),
                    "limiter": tr.get("limiter"), "limiter_frac": tr.get("limiter_frac"),
                    "capture": tr.get("source"), "capture_poses": tr.get("poses")}
     except (OSError, KeyError, ValueError):
         pass
     achieved = bytes_8d / (kms["fj"] / 1e3) / 1e9
     lts_gbs = (ncu["lts_bytes"] / (kms["fj"] / 1e3) / 1e9) if ncu.get("lts_bytes") else None
+    # the north star's "ncu gather bandwidth": the 32-B sectors the gathers are
+    # served at (L1 hits + misses) and the part of them that comes from L2
+    gather_gbs = (ncu["gather_sector_bytes"] / (kms["fj"] / 1e3) / 1e9
+                  if ncu.get("gather_sector_bytes") else None)
+    l2sm_gbs = (ncu["l2_to_sm_bytes"] / (kms["fj"] / 1e3) / 1e9
+                if ncu.get("l2_to_sm_bytes") else None)
 
     if world > 1:
         dist.barrier()
@@ -602,6 +612,15 @@ def main():
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": ncu.get("traffic"),
                      "lts_gbs": lts_gbs,
+                     "gather_bw": {"l1_sectors_gbs": gather_gbs,
+                                   "l1_sectors_frac_of_hbm": (gather_gbs / hbm_peak
+                                                              if gather_gbs else None),
+                                   "l2_to_sm_gbs": l2sm_gbs,
+                                   "l2_to_sm_frac_of_hbm": (l2sm_gbs / hbm_peak
+                                                            if l2sm_gbs else None),
+                                   "rule": "ncu l1tex__t_sectors_pipe_lsu_mem_global_op_ld x 32 B "
+                                           "and l1tex__m_xbar2l1tex_read_bytes per launch (the "
+                                           "capture, scaled per pose) / this run's launch time"},
                      "algorithmic_bytes_per_launch": bytes_8d,
                      "gathered_bytes_per_launch": bytes_walk,
                      "frac_gathered": bytes_walk / (kms["fj"] / 1e3) / 1e9 / hbm_peak,
