@@ -335,8 +335,11 @@ def count_steps(vol: DeviceVolume, det: Detector, frames: torch.Tensor,
 
 
 # Above this many bytes of stored ray Jacobian, autograd re-walks the rays in
-# backward instead (drr_backward) -- e.g. 64 poses at 1024^2 would hold 3.2 GB.
-JAC_BUDGET_BYTES = 2 << 30
+# backward instead (drr_backward) and batched loss_and_gradient takes the fused
+# walk.  8 GiB (4.4% of a B200's HBM) keeps C5 (64 poses at 1024^2: 3.2 GB) on
+# the stored-Jacobian chain: 53.9 ms vs 56.6 for the fused walk
+# (scripts/c5_modes.py, profiles/r02/SUMMARY.md).
+JAC_BUDGET_BYTES = 8 << 30
 
 
 class _RenderFrames(torch.autograd.Function):
