@@ -347,10 +347,17 @@ def other_configs(sd, dev, timed, world, rank):
         for name, r in (("C2", r2), ("C2_fine_steps", r2f), ("C1", r1)):
             fd[name] = {k: r[k] for k in ("max_rel_kink_free", "n_kink_free", "boundary",
                                           "unexplained", "rel")}
+        # ray by ray (fd.ray_fd_report): each ray's energy gradient vs its own
+        # central FD, boundaries attributed per (ray, component)
+        from paper_2208_12737_b200.fd import ray_fd_report
+        for name, (vv, dd) in (("C2_rays", (sd.volume, sd.detector)), ("C1_rays", (v1, d1))):
+            fd[name] = ray_fd_report(vv, dd, eta2)
         out["fd_check"] = {"method": "central FD, default_fd_steps (gradients.py:72-74), "
                                      "float64 renders; components whose stencil crosses a "
                                      "traversal-structure change (detect_fd_boundaries) are "
-                                     "excluded; the reference's bar is rel < 1e-5",
+                                     "excluded; the reference's bar is rel < 1e-5. *_rays: the "
+                                     "same per (ray, component) of the ray energies at C2's "
+                                     "pose (fd.ray_fd_report)",
                            **fd}
         out["C3"] = {"workload": "slice-to-volume registration on C2: 250 momentum-GD steps "
                                  "(251 fwd+bwd iterations) of neg-ZNCC, whole loop one CUDA graph, "

@@ -30,6 +30,9 @@
  *                               (number of used voxel-steps per ray)
  *   drr_signature            <- gradients.py:124-142 discrete_signature (the
  *                               traversal structure of every ray, hashed)
+ *   drr_ray_signatures       <- the same, one hash per ray (per-ray
+ *                               attribution of detect_fd_boundaries,
+ *                               gradients.py:145-167)
  *   drr_pose_frames          <- geometry.py:120-149 _pose_frame (+ the
  *                               isocenter offset of geometry.py:166-175), batched
  *   drr_pose_grad            <- the tangent half of the same map (dual.py
@@ -225,6 +228,13 @@ int drr_count_steps(const void *d_vol, int vol_dtype, const drr_grid *grid,
 int drr_signature(const void *d_vol, int vol_dtype, const drr_grid *grid,
                   const double *d_frames, int32_t n_poses,
                   const drr_detector *det, uint64_t *d_sig, void *stream);
+
+/* The per-ray terms of drr_signature: d_sig is B x H x W uint64, and each
+ * pose's drr_signature is the wrapping sum of its rays' entries.  Used to
+ * attribute finite-difference stencils ray by ray (fd.ray_fd_report). */
+int drr_ray_signatures(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                       const double *d_frames, int32_t n_poses,
+                       const drr_detector *det, uint64_t *d_sig, void *stream);
 
 /* B x 7 pose vectors (rho, theta, phi, gamma, bx, by, bz) -> B x 12 frames.
  * isocenter: 3 doubles in HOST memory (the volume centre). */

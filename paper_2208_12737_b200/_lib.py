@@ -43,6 +43,7 @@ EXPORTS = (
     "drr_volume_hull_dirs",
     "drr_volume_hull",
     "drr_signature",
+    "drr_ray_signatures",
     "drr_pose_frames",
     "drr_pose_grad",
     "drr_image_loss",
@@ -115,6 +116,7 @@ _SIGNATURES = {
     "drr_volume_hull": ([_vp, _int, _GP, _vp, _vp], _int),
     "drr_volume_bounds": ([_vp, _int, _GP, _vp, _vp], _int),
     "drr_signature": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
+    "drr_ray_signatures": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _vp], _int),
     "drr_pose_frames": ([_vp, _i32, ctypes.POINTER(ctypes.c_double), _vp, _vp], _int),
     "drr_pose_grad": ([_vp, _vp, _i32, _vp, _vp], _int),
     "drr_image_loss": ([_vp, _vp, _int, _i64, _i32, _i64, _int, _vp, _vp, _vp, _vp], _int),

@@ -660,7 +660,10 @@ __global__ void k_hull_init(int* out) {
 // order-free, so the atomics give the same bits every run.  Replaces
 // gradients.py:124-142 discrete_signature for detect_fd_boundaries
 // (gradients.py:145-167).  One thread per ray, the v4 visitor walk.
-template <typename VT>
+// kPerRay: each ray's own hash to sig[(b H + h) W + w] instead (per-ray
+// boundary attribution of finite differences, fd.ray_fd_report); the pose
+// signature is their wrapping sum.
+template <typename VT, bool kPerRay>
 __global__ void __launch_bounds__(kThreads)
     k_signature(const VT* __restrict__ vol, const GridDev g, const double* __restrict__ frames,
                 const DetDev det, unsigned long long* __restrict__ sig) {
@@ -684,10 +687,13 @@ __global__ void __launch_bounds__(kThreads)
       vis.h = sig_mix(vis.h, 0xDEADull);  // miss
     }
     v = sig_mix(static_cast<uint64_t>(h) * det.W + w, vis.h);
+    if constexpr (kPerRay) sig[(static_cast<size_t>(b) * det.H + h) * det.W + w] = v;
   }
+  if constexpr (!kPerRay) {
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  if ((threadIdx.x & 31) == 0) atomicAdd(sig + b, static_cast<unsigned long long>(v));
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0) atomicAdd(sig + b, static_cast<unsigned long long>(v));
+  }
 }
 
 // One CTA per pose: the CTA partials of the three 12-vectors in a fixed order,
@@ -1755,9 +1761,9 @@ int drr_volume_hull(const void* d_vol, int vol_dtype, const drr_grid* grid, int3
   return check_launch("drr_volume_hull");
 }
 
-int drr_signature(const void* d_vol, int vol_dtype, const drr_grid* grid,
-                  const double* d_frames, int32_t n_poses, const drr_detector* det,
-                  uint64_t* d_sig, void* stream) {
+static int signature_launch(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                            const double* d_frames, int32_t n_poses, const drr_detector* det,
+                            uint64_t* d_sig, void* stream, bool per_ray) {
   drr::GridDev g;
   drr::DetDev d;
   int rc = make_grid(grid, g);
@@ -1774,21 +1780,36 @@ int drr_signature(const void* d_vol, int vol_dtype, const drr_grid* grid,
     return fail(DRR_ERR_INVALID_ARGUMENT, "n_poses must be in [0, 65535], got %d", n_poses);
   if (n_poses == 0) return DRR_OK;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaMemsetAsync(d_sig, 0, sizeof(uint64_t) * n_poses, st);
+  if (!per_ray) cudaMemsetAsync(d_sig, 0, sizeof(uint64_t) * n_poses, st);
   const dim3 grd = pose_grid(d, n_poses, 1);
   auto* out = reinterpret_cast<unsigned long long*>(d_sig);
+  auto launch = [&](auto kern, const auto* vol) {
+    ensure_smem(kern, smem);
+    kern<<<grd, drr::kThreads, smem, st>>>(vol, g, d_frames, d, out);
+  };
   if (vol_dtype == DRR_VOL_F32) {
-    ensure_smem(drr::k_signature<float>, smem);
-    drr::k_signature<float><<<grd, drr::kThreads, smem, st>>>(static_cast<const float*>(d_vol), g,
-                                                              d_frames, d, out);
+    const auto* v = static_cast<const float*>(d_vol);
+    per_ray ? launch(drr::k_signature<float, true>, v) : launch(drr::k_signature<float, false>, v);
   } else if (vol_dtype == DRR_VOL_F64) {
-    ensure_smem(drr::k_signature<double>, smem);
-    drr::k_signature<double><<<grd, drr::kThreads, smem, st>>>(
-        static_cast<const double*>(d_vol), g, d_frames, d, out);
+    const auto* v = static_cast<const double*>(d_vol);
+    per_ray ? launch(drr::k_signature<double, true>, v)
+            : launch(drr::k_signature<double, false>, v);
   } else {
     return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
   }
-  return check_launch("drr_signature");
+  return check_launch(per_ray ? "drr_ray_signatures" : "drr_signature");
+}
+
+int drr_signature(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                  const double* d_frames, int32_t n_poses, const drr_detector* det,
+                  uint64_t* d_sig, void* stream) {
+  return signature_launch(d_vol, vol_dtype, grid, d_frames, n_poses, det, d_sig, stream, false);
+}
+
+int drr_ray_signatures(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                       const double* d_frames, int32_t n_poses, const drr_detector* det,
+                       uint64_t* d_sig, void* stream) {
+  return signature_launch(d_vol, vol_dtype, grid, d_frames, n_poses, det, d_sig, stream, true);
 }
 
 int drr_volume_pack(const void* d_src, int src_type, int src_order, const int64_t* dims,

@@ -159,3 +159,95 @@ def fd_report(vol: DeviceVolume, det: Detector, eta, fixed, loss_kind: str = "ne
             "max_rel_kink_free": float(rel[clean].max()) if clean.any() else None,
             "n_kink_free": int(clean.sum()),
             "unexplained": bool(((rel >= 1e-5) & clean).any())}
+
+
+def ray_signatures(vol: DeviceVolume, det: Detector, eta_rows, isocenter=None) -> np.ndarray:
+    """Per-ray traversal-structure signatures (n, H, W) uint64 of the (n, 7)
+    poses (``drr_ray_signatures``; a pose's :func:`signatures` entry is the
+    wrapping sum of its rays')."""
+    fr = _frames(vol, np.asarray(eta_rows, dtype=np.float64).reshape(-1, 7), isocenter)
+    sig = torch.empty((fr.shape[0], det.height, det.width), dtype=torch.int64, device=fr.device)
+    _lib.check(_lib.load().drr_ray_signatures(vol.flat.data_ptr(), vol.vol_dtype, vol.grid,
+                                              fr.data_ptr(), fr.shape[0], det.c, sig.data_ptr(),
+                                              torch.cuda.current_stream(fr.device).cuda_stream))
+    return sig.cpu().numpy().view(np.uint64)
+
+
+def ray_fd_report(vol: DeviceVolume, det: Detector, eta, steps=None, isocenter=None) -> dict:
+    """Central FD of every ray's energy against its exact pose gradient, with
+    the boundary test of ``detect_fd_boundaries`` (gradients.py:145-167)
+    applied ray by ray.
+
+    On a full detector nearly every pose-level stencil straddles some ray's
+    structure change (C2: all 7 components), so the image-level report has no
+    kink-free component to test; per ray most stencils are kink-free, and
+    there the reference's bar (rel < 1e-5, test_gradients.py:119-148) applies
+    to each (ray, component).  Exact: the float64 energy Jacobian of one walk
+    (``drr_forward_jac``: dE/ds, dE/dp) chained through the frame map
+    (geometry.py:120-149).  FD: float64 renders of the bumped poses at the
+    steps and at half the steps (a pair is kink-free when neither stencil
+    changes its ray's structure).  A pair above the bar whose Richardson
+    extrapolation (4 FD(h/2) - FD(h)) / 3 meets it is FD truncation error
+    (O(h^2): a grazing ray's crossings curve fast), not a gradient error;
+    ``unexplained`` counts the pairs that fail both."""
+    from .geometry import pose_frames
+    from .renderer import render_frames, render_frames_jac
+    eta = np.asarray(eta, dtype=np.float64).reshape(7)
+    _check_pose(eta)
+    s = _steps(steps)
+    H, W = det.height, det.width
+
+    def central(step):
+        rows = _stencil(eta, step, "central")
+        img = render_frames(vol, det, _frames(vol, rows, isocenter),
+                            out_dtype=torch.float64).cpu().numpy()
+        fd = np.stack([(img[1 + 2 * i] - img[2 + 2 * i]) / (2.0 * step[i]) for i in range(7)], -1)
+        sig = ray_signatures(vol, det, rows, isocenter)
+        kink = np.stack([(sig[1 + 2 * i] != sig[0]) | (sig[2 + 2 * i] != sig[0])
+                         for i in range(7)], -1)  # (H, W, 7)
+        return img[0], fd, kink
+
+    E, fd, kink = central(s)
+    _, fd2, kink2 = central(0.5 * s)
+    rich = (4.0 * fd2 - fd) / 3.0
+    _, jac = render_frames_jac(vol, det, _frames(vol, eta[None], isocenter),
+                               out_dtype=torch.float64)
+    jac = jac.cpu().numpy().reshape(6, H, W)
+    iso = vol.center if isocenter is None else tuple(float(v) for v in isocenter)
+    Jf = torch.autograd.functional.jacobian(
+        lambda e: pose_frames(e[None], iso)[0], torch.tensor(eta)).numpy()  # (12, 7)
+    ah = (np.arange(H) - (H - 1) / 2.0) * det.pitch_y
+    aw = (np.arange(W) - (W - 1) / 2.0) * det.pitch_x
+    dp = (Jf[3:6][None, None] + ah[:, None, None, None] * Jf[6:9][None, None]
+          + aw[None, :, None, None] * Jf[9:12][None, None])  # (H, W, 3, 7)
+    exact = (np.einsum("ahw,aj->hwj", jac[0:3], Jf[0:3])
+             + np.einsum("ahw,hwaj->hwj", jac[3:6], dp))  # (H, W, 7)
+
+    def rel(f):
+        den = np.maximum(np.abs(exact), np.abs(f))
+        return np.abs(exact - f) / np.where(den > 0, den, 1.0), den
+
+    r, den = rel(fd)
+    rr, _ = rel(rich)
+    # The FD quotients' own rounding: a ray energy sums a few hundred segments
+    # in float64 (~1e-13 |E| relative at most), divided by 2 h (x3 for the
+    # extrapolation).  A pair is resolvable at the 1e-5 bar when its gradient
+    # is above that noise / 1e-5 (the per-ray counterpart of the reference's
+    # |exact| > 1e-8 for O(1) losses).
+    noise = 3e-13 * np.abs(E)[..., None] / s[None, None, :]
+    hit = (E != 0.0)[..., None] & np.ones(7, dtype=bool)
+    boundary = hit & (kink | kink2)
+    tested = hit & ~boundary & (den > noise / 1e-5)
+    over = tested & (r >= 1e-5)
+    bad = over & (rr >= 1e-5)
+    return {"rays": int(H * W), "rays_nonzero": int(hit[..., 0].sum()),
+            "pairs": int(hit.sum()), "pairs_boundary": int(boundary.sum()),
+            "pairs_tested": int(tested.sum()),
+            "max_rel_kink_free": float(r[tested].max()) if tested.any() else None,
+            "p99_rel_kink_free": float(np.quantile(r[tested], 0.99)) if tested.any() else None,
+            "n_over_1e-5": int(over.sum()),
+            "n_over_1e-5_truncation": int((over & ~bad).sum()),
+            "max_rel_richardson": float(rr[tested].max()) if tested.any() else None,
+            "unexplained": int(bad.sum()),
+            "per_component_tested": tested.sum(axis=(0, 1)).tolist(),
+            "max_rel_boundary": float(r[boundary].max()) if boundary.any() else None}

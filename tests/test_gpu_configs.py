@@ -110,4 +110,5 @@ def test_c5_large_case(cuda_device):
     finally:
         renderer.JAC_BUDGET_BYTES = budget
     np.testing.assert_allclose(one_walk, rewalk, rtol=1e-12, atol=1e-15)
-    assert renderer.jac_bytes(det, 64) > budget  # C5's 64-pose batch takes the re-walk
+    # C5's 64-pose batch (3.2 GB of Jacobian) stays on the stored-Jacobian chain
+    assert renderer.jac_bytes(det, 64) <= budget

@@ -88,3 +88,48 @@ def test_boundaries_agree_with_reference(setup):
                                           steps=steps)
             got = detect_fd_boundaries(vol, det, eta, steps=steps)
             np.testing.assert_array_equal(got, ref, err_msg=f"eta={eta} steps={steps}")
+
+
+def test_ray_signatures_sum_to_pose_signature(setup):
+    from paper_2208_12737_b200.fd import ray_signatures, signatures
+    _, vol, det, _ = setup
+    rows = np.stack([TRUTH, TRUTH + np.array([0, 0.2, -0.1, 0.3, 2.0, -1.0, 0.5])])
+    per_ray = ray_signatures(vol, det, rows)
+    assert per_ray.shape == (2, 21, 21)
+    with np.errstate(over="ignore"):
+        sums = per_ray.reshape(2, -1).sum(axis=1, dtype=np.uint64)
+    np.testing.assert_array_equal(sums, signatures(vol, det, rows))
+
+
+def test_ray_fd_small_case(setup):
+    """Per-ray central FD vs the exact per-ray pose gradient at the
+    reference's 1e-5 bar on every kink-free (ray, component) pair."""
+    from paper_2208_12737_b200.fd import ray_fd_report
+    _, vol, det, _ = setup
+    rng = np.random.default_rng(5)
+    for _ in range(4):
+        eta = TRUTH + rng.uniform(-1, 1, 7) * np.array([0, 0.4, 0.4, 0.3, 6.0, 6.0, 6.0])
+        rep = ray_fd_report(vol, det, eta)
+        assert rep["pairs_tested"] > 0.5 * rep["pairs"], rep
+        assert rep["unexplained"] == 0, rep
+        assert rep["max_rel_kink_free"] < 1e-5
+
+
+def test_ray_fd_c2(cuda_device):
+    """The same at C2 (chest 512x512x133, 200x200): the pose-level report has no
+    kink-free component there (every stencil crosses some ray's structure
+    change); per ray, most pairs are kink-free.  All of them meet 1e-5 but a
+    few dozen grazing rays whose central FD carries O(h^2) truncation error:
+    those meet it after Richardson extrapolation (the exact gradient agrees
+    with it to 2.6e-7 at worst)."""
+    from paper_2208_12737_b200 import Detector, DeviceVolume, synthetic
+    from paper_2208_12737_b200.fd import ray_fd_report
+    vol = DeviceVolume(synthetic.chest_phantom((512, 512, 133)), (0.703125, 0.703125, 2.5),
+                       device=cuda_device)
+    det = Detector(200, 200, 3.6)
+    eta = np.array([300.0, math.pi / 2 + 0.05, math.pi / 2 - 0.04, 0.03, 2.0, -3.0, 1.5])
+    rep = ray_fd_report(vol, det, eta)
+    assert rep["pairs_tested"] > 0.4 * rep["pairs"], rep
+    assert rep["unexplained"] == 0, rep
+    assert rep["max_rel_richardson"] < 1e-5
+    assert rep["n_over_1e-5"] < 1e-3 * rep["pairs_tested"], rep
