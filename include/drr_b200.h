@@ -14,6 +14,10 @@
  *                               (and jacobs_raysum, _native.pyx:285-382: the
  *                               GPU walk is already incremental)
  *   drr_raysum_endpoint_grad <- _kernels/_native.pyx:196-282 siddon_raysum_grad
+ *                               (reverse-mode: dE/ds, dE/dp per ray)
+ *   drr_raysum_tangents      <- the same function with its own contract:
+ *                               energies + d_energy (N x T) from the caller's
+ *                               source / pixel tangents
  *                               (reverse-mode form: dE/ds, dE/dp per ray; the
  *                               host shim contracts them with the T tangents)
  *   drr_forward              <- raytrace.py:132-142 render() fused with
@@ -144,6 +148,16 @@ int drr_raysum_endpoint_grad(const void *d_vol, int vol_dtype,
                              const double *d_pix, int64_t n_rays,
                              double *d_out, double *d_dEds, double *d_dEdp,
                              void *stream);
+
+/* siddon_raysum_grad's own contract (_native.pyx:196-282): energies and
+ * d_energy[r, t] = dE/ds . d_src[:, t] + dE/dp . d_pix[r, :, t], the
+ * endpoint derivatives contracted in the walk's epilogue.  d_dsrc: 3 x T,
+ * d_dpix: N x 3 x T, d_denergy: N x T (row-major doubles). */
+int drr_raysum_tangents(const void *d_vol, int vol_dtype, const drr_grid *grid,
+                        const double *d_src, const double *d_dsrc,
+                        const double *d_pix, const double *d_dpix,
+                        int64_t n_rays, int32_t n_tangents, double *d_out,
+                        double *d_denergy, void *stream);
 
 /* Batched DRR forward: pixel rays generated in-kernel from the frames.
  * d_img: B x H x W, float32 (img_dtype 0) or float64 (img_dtype 1). */

@@ -32,6 +32,7 @@ EXPORTS = (
     "drr_struct_sizes",
     "drr_raysum",
     "drr_raysum_endpoint_grad",
+    "drr_raysum_tangents",
     "drr_forward",
     "drr_backward_workspace_size",
     "drr_backward",
@@ -105,6 +106,8 @@ _SIGNATURES = {
     "drr_struct_sizes": ([_vp, _vp, _vp, _vp], _int),
     "drr_raysum": ([_vp, _int, _GP, _vp, _vp, _i64, _vp, _vp], _int),
     "drr_raysum_endpoint_grad": ([_vp, _int, _GP, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _int),
+    "drr_raysum_tangents": ([_vp, _int, _GP, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp],
+                            _int),
     "drr_forward": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp], _int),
     "drr_backward_workspace_size": ([_i32, _DP], _sz),
     "drr_backward": ([_vp, _int, _GP, _vp, _i32, _DP, _vp, _int, _vp, _vp, _int, _vp, _sz, _vp], _int),

@@ -9,9 +9,9 @@ module has exactly that surface, so the reference's callers
 (``test_kernel_properties.py``) run unchanged against the GPU:
 
 * ``siddon_raysum``      -> ``drr_raysum`` (one CUDA walk per ray);
-* ``siddon_raysum_grad`` -> ``drr_raysum_endpoint_grad`` + the contraction
-  d_energy[r, t] = dE/ds_r . d_source[:, t] + dE/dp_r . d_pixels[r, :, t]
-  (on the device, torch f64);
+* ``siddon_raysum_grad`` -> ``drr_raysum_tangents``: the walk's reverse-mode
+  endpoint derivatives contracted in its epilogue,
+  d_energy[r, t] = dE/ds_r . d_source[:, t] + dE/dp_r . d_pixels[r, :, t];
 * ``jacobs_raysum``      -> the same walk: the GPU traversal already advances
   plane by plane, so the reference's iterative oracle and its vectorised
   kernel coincide here (the reference requires them to agree within 1e-9,
@@ -27,11 +27,14 @@ The reference's dispatchers call a backend once per chunk of rays
 same ``volume.flat_data()`` each time, so the device copy of a READ-ONLY flat
 volume (the reference's ``Volume`` freezes its data, ``volume.py:52``) is
 cached, keyed on its buffer and geometry; a writeable array is uploaded on
-every call (its contents may change between calls).
+every call (its contents may change between calls).  Each chunk's rays and
+tangents go up in one pinned copy and its outputs come back in one
+(``_Staging``).
 """
 
 from __future__ import annotations
 
+import threading
 import warnings
 
 import numpy as np
@@ -87,42 +90,107 @@ def _bounds(vol, dims):
                          _lib.DRR_VOL_F64, hull=True)
 
 
+class _Staging:
+    """Persistent pinned host and device buffers for the per-chunk transfers.
+
+    The reference's dispatchers call a backend once per chunk (~20 calls for
+    one 200 x 200 ``render_with_gradient``), so each call packs its inputs
+    into one pinned buffer, moves them with ONE host-to-device copy, runs ONE
+    launch and reads the outputs back with ONE device-to-host copy -- no
+    per-call allocations.  Buffers grow to the largest chunk seen."""
+
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.dev = None
+        self.h_in = self.h_out = self.d_in = self.d_out = None
+
+    def _fit(self, dev, n_in, n_out):
+        if self.dev != dev or self.h_in is None or self.h_in.numel() < n_in:
+            self.h_in = torch.empty(max(n_in, 1024), dtype=torch.float64, pin_memory=True)
+            self.d_in = torch.empty(self.h_in.numel(), dtype=torch.float64, device=dev)
+        if self.dev != dev or self.h_out is None or self.h_out.numel() < n_out:
+            self.h_out = torch.empty(max(n_out, 1024), dtype=torch.float64, pin_memory=True)
+            self.d_out = torch.empty(self.h_out.numel(), dtype=torch.float64, device=dev)
+        self.dev = dev
+
+    def run(self, dev, inputs, n_out, launch):
+        """inputs: float64 arrays packed in order; launch(device pointers of
+        the inputs, device pointer of the output area, stream); returns the
+        first n_out doubles of the output area as a fresh numpy array."""
+        sizes = [a.size for a in inputs]
+        n_in = int(sum(sizes))
+        with self.lock:
+            self._fit(dev, n_in, n_out)
+            h = self.h_in.numpy()
+            ptrs, off = [], 0
+            base = self.d_in.data_ptr()
+            for a, n in zip(inputs, sizes):
+                h[off:off + n] = a.reshape(-1)
+                ptrs.append(base + 8 * off)
+                off += n
+            stream = torch.cuda.current_stream(dev)
+            self.d_in[:n_in].copy_(self.h_in[:n_in], non_blocking=True)
+            launch(ptrs, self.d_out.data_ptr(), stream.cuda_stream)
+            self.h_out[:n_out].copy_(self.d_out[:n_out], non_blocking=True)
+            stream.synchronize()
+            return self.h_out[:n_out].numpy().copy()
+
+
+_STAGING = _Staging()
+# (dims, spacing, origin, box, hull) -> drr_grid: the chunks of one call share it
+_GRIDS: dict = {}
+
+
+def _grid(dims, spacing, origin, occupied, hull):
+    key = (tuple(int(n) for n in dims), tuple(float(v) for v in np.broadcast_to(spacing, 3)),
+           tuple(float(v) for v in np.broadcast_to(origin, 3)), occupied,
+           None if hull is None else (tuple(hull[0]), tuple(hull[1])))
+    g = _GRIDS.get(key)
+    if g is None:
+        if len(_GRIDS) > 8:
+            _GRIDS.clear()
+        g = _GRIDS[key] = _lib.make_grid(dims, spacing, origin, occupied, hull)
+    return g
+
+
 def _prep(flat_data, dims, spacing, origin, source, pixels):
     dev = _device()
     pix = np.ascontiguousarray(np.atleast_2d(pixels), dtype=np.float64)
     vol, (occupied, hull) = _device_volume(flat_data, dims, dev)
-    grid = _lib.make_grid(dims, spacing, origin, occupied, hull)
-    src = _upload(np.asarray(source).reshape(3), dev)
-    return dev, grid, vol, src, _upload(pix, dev), pix.shape[0]
+    src = np.ascontiguousarray(np.asarray(source, dtype=np.float64).reshape(3))
+    return dev, _grid(dims, spacing, origin, occupied, hull), vol, src, pix, pix.shape[0]
 
 
 def siddon_raysum(flat_data, dims, spacing, origin, source, pixels):
     """Energies (N,) float64 -- contract of ``_native.siddon_raysum``."""
     dev, grid, vol, src, pix, n = _prep(flat_data, dims, spacing, origin, source, pixels)
-    out = torch.empty(n, dtype=torch.float64, device=dev)
+    if n == 0:
+        return np.zeros(0)
     lib = _lib.load()
-    _lib.check(lib.drr_raysum(vol.data_ptr(), _lib.DRR_VOL_F64, grid, src.data_ptr(),
-                              pix.data_ptr(), n, out.data_ptr(),
-                              torch.cuda.current_stream(dev).cuda_stream))
-    return out.cpu().numpy()
+
+    def launch(p, out, st):
+        _lib.check(lib.drr_raysum(vol.data_ptr(), _lib.DRR_VOL_F64, grid, p[0], p[1], n, out, st))
+    return _STAGING.run(dev, (src, pix), n, launch)
 
 
 def siddon_raysum_grad(flat_data, dims, spacing, origin, source, d_source,
                        pixels, d_pixels):
-    """(energy (N,), d_energy (N, T)) -- contract of ``_native.siddon_raysum_grad``."""
+    """(energy (N,), d_energy (N, T)) -- contract of ``_native.siddon_raysum_grad``
+    (``drr_raysum_tangents``: the walk with the tangent contraction in its
+    epilogue)."""
     dev, grid, vol, src, pix, n = _prep(flat_data, dims, spacing, origin, source, pixels)
-    out = torch.empty(n, dtype=torch.float64, device=dev)
-    dEds = torch.empty((n, 3), dtype=torch.float64, device=dev)
-    dEdp = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    dsrc = np.ascontiguousarray(d_source, dtype=np.float64).reshape(3, -1)
+    T = dsrc.shape[1]
+    dpix = np.ascontiguousarray(d_pixels, dtype=np.float64).reshape(n, 3, T)
+    if n == 0:
+        return np.zeros(0), np.zeros((0, T))
     lib = _lib.load()
-    _lib.check(lib.drr_raysum_endpoint_grad(
-        vol.data_ptr(), _lib.DRR_VOL_F64, grid, src.data_ptr(), pix.data_ptr(), n,
-        out.data_ptr(), dEds.data_ptr(), dEdp.data_ptr(),
-        torch.cuda.current_stream(dev).cuda_stream))
-    dsrc = _upload(d_source, dev)                              # (3, T)
-    dpix = _upload(d_pixels, dev).reshape(n, 3, -1)            # (N, 3, T)
-    d_energy = dEds @ dsrc + torch.einsum("na,nat->nt", dEdp, dpix)
-    return out.cpu().numpy(), d_energy.cpu().numpy()
+
+    def launch(p, out, st):
+        _lib.check(lib.drr_raysum_tangents(vol.data_ptr(), _lib.DRR_VOL_F64, grid, p[0], p[1],
+                                           p[2], p[3], n, T, out, out + 8 * n, st))
+    res = _STAGING.run(dev, (src, dsrc, pix, dpix), n * (1 + T), launch)
+    return res[:n].copy(), res[n:].reshape(n, T)
 
 
 def jacobs_raysum(flat_data, dims, spacing, origin, source, pixels):
@@ -133,12 +201,12 @@ def jacobs_raysum(flat_data, dims, spacing, origin, source, pixels):
 def ray_endpoint_grad(flat_data, dims, spacing, origin, source, pixels):
     """(energy, dE/ds (N, 3), dE/dp (N, 3)) -- the reverse-mode form."""
     dev, grid, vol, src, pix, n = _prep(flat_data, dims, spacing, origin, source, pixels)
-    out = torch.empty(n, dtype=torch.float64, device=dev)
-    dEds = torch.empty((n, 3), dtype=torch.float64, device=dev)
-    dEdp = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    if n == 0:
+        return np.zeros(0), np.zeros((0, 3)), np.zeros((0, 3))
     lib = _lib.load()
-    _lib.check(lib.drr_raysum_endpoint_grad(
-        vol.data_ptr(), _lib.DRR_VOL_F64, grid, src.data_ptr(), pix.data_ptr(), n,
-        out.data_ptr(), dEds.data_ptr(), dEdp.data_ptr(),
-        torch.cuda.current_stream(dev).cuda_stream))
-    return out.cpu().numpy(), dEds.cpu().numpy(), dEdp.cpu().numpy()
+
+    def launch(p, out, st):
+        _lib.check(lib.drr_raysum_endpoint_grad(vol.data_ptr(), _lib.DRR_VOL_F64, grid, p[0], p[1],
+                                                n, out, out + 8 * n, out + 32 * n, st))
+    res = _STAGING.run(dev, (src, pix), 7 * n, launch)
+    return res[:n].copy(), res[n:4 * n].reshape(n, 3).copy(), res[4 * n:].reshape(n, 3).copy()

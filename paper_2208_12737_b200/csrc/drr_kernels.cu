@@ -1043,13 +1043,21 @@ __global__ void __launch_bounds__(kRayThreads)
   out[i] = e;
 }
 
+// With n_tan > 0 (drr_raysum_tangents) the epilogue contracts the endpoint
+// derivatives with the caller's tangents instead of storing them:
+// d_energy[i, t] = dE/ds . d_source[:, t] + dE/dp . d_pixels[i, :, t]
+// (the reference's siddon_raysum_grad contract, _native.pyx:196-282), in a
+// fixed order per (ray, tangent).
 template <typename VT>
 __global__ void __launch_bounds__(kRayThreads)
     k_raysum_grad(const VT* __restrict__ vol, const GridDev g,
                   const double* __restrict__ src,
                   const double* __restrict__ pix, int64_t n_rays,
                   double* __restrict__ out, double* __restrict__ dEds,
-                  double* __restrict__ dEdp) {
+                  double* __restrict__ dEdp, int n_tan = 0,
+                  const double* __restrict__ dsrc = nullptr,
+                  const double* __restrict__ dpix = nullptr,
+                  double* __restrict__ denergy = nullptr) {
   extern __shared__ __align__(16) double tab[];
   build_plane_table(g, src, tab);
   __syncthreads();
@@ -1069,6 +1077,19 @@ __global__ void __launch_bounds__(kRayThreads)
     sums_to_endpoint_grads(r, o.acc, G, Hh, L, gs, gp);
   }
   out[i] = e;
+  if (n_tan > 0) {
+    const double* dp = dpix + 3 * i * n_tan;
+    for (int t = 0; t < n_tan; ++t) {
+      double v = gs[0] * __ldg(dsrc + t);
+      v = v + gs[1] * __ldg(dsrc + n_tan + t);
+      v = v + gs[2] * __ldg(dsrc + 2 * n_tan + t);
+      v = v + gp[0] * __ldg(dp + t);
+      v = v + gp[1] * __ldg(dp + n_tan + t);
+      v = v + gp[2] * __ldg(dp + 2 * n_tan + t);
+      denergy[i * n_tan + t] = v;
+    }
+    return;
+  }
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     dEds[3 * i + a] = gs[a];
@@ -1482,6 +1503,36 @@ int drr_raysum_endpoint_grad(const void* d_vol, int vol_dtype,
   else
     return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
   return check_launch("drr_raysum_endpoint_grad");
+}
+
+int drr_raysum_tangents(const void* d_vol, int vol_dtype, const drr_grid* grid,
+                        const double* d_src, const double* d_dsrc, const double* d_pix,
+                        const double* d_dpix, int64_t n_rays, int32_t n_tangents,
+                        double* d_out, double* d_denergy, void* stream) {
+  drr::GridDev g;
+  int rc = make_grid(grid, g);
+  if (rc) return rc;
+  const size_t smem = table_bytes(g, true);
+  if (n_rays < 0) return fail(DRR_ERR_INVALID_ARGUMENT, "n_rays < 0");
+  if (n_tangents < 1)
+    return fail(DRR_ERR_INVALID_ARGUMENT, "n_tangents must be >= 1, got %d", n_tangents);
+  if (n_rays == 0) return DRR_OK;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const unsigned blocks = static_cast<unsigned>((n_rays + drr::kRayThreads - 1) / drr::kRayThreads);
+  if (vol_dtype == DRR_VOL_F32) {
+    ensure_smem(drr::k_raysum_grad<float>, smem);
+    drr::k_raysum_grad<float><<<blocks, drr::kRayThreads, smem, st>>>(
+        static_cast<const float*>(d_vol), g, d_src, d_pix, n_rays, d_out, nullptr, nullptr,
+        n_tangents, d_dsrc, d_dpix, d_denergy);
+  } else if (vol_dtype == DRR_VOL_F64) {
+    ensure_smem(drr::k_raysum_grad<double>, smem);
+    drr::k_raysum_grad<double><<<blocks, drr::kRayThreads, smem, st>>>(
+        static_cast<const double*>(d_vol), g, d_src, d_pix, n_rays, d_out, nullptr, nullptr,
+        n_tangents, d_dsrc, d_dpix, d_denergy);
+  } else {
+    return fail(DRR_ERR_INVALID_ARGUMENT, "unknown vol_dtype %d", vol_dtype);
+  }
+  return check_launch("drr_raysum_tangents");
 }
 
 int drr_forward(const void* d_vol, int vol_dtype, const drr_grid* grid,

@@ -88,7 +88,7 @@ def volume_bounds(flat: torch.Tensor, grid, vol_dtype: int, hull: bool = False):
 
 def trim_grid(flat: torch.Tensor, dims, spacing, origin, vol_dtype: int, trim=True):
     """(grid, occupied box, hull) for a device volume: ``trim`` True = the box
-    and the 10-direction hull, "box" = the box only, False = the whole volume."""
+    and the 14-direction hull, "box" = the box only, False = the whole volume."""
     grid = _lib.make_grid(dims, spacing, origin)
     if not trim or flat.numel() == 0:
         return grid, None, None

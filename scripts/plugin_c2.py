@@ -45,6 +45,16 @@ for backend in ("cuda", "native"):
             t.append(time.perf_counter() - t0)
         res[(backend, name)] = r
         out[f"{backend}_{name}_ms"] = 1e3 * float(np.median(t))
+# the reference's own host work inside those calls (pixel grids and their
+# tangents, gradients.py / geometry.py): the floor any backend sits on
+for name, fn in (("detector_grid", lambda: dt.detector_grid(pose, spec)),
+                 ("detector_grid_with_tangents", lambda: dt.detector_grid_with_tangents(pose, spec))):
+    t = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        fn()
+        t.append(time.perf_counter() - t0)
+    out[f"host_{name}_ms"] = 1e3 * float(np.median(t))
 img_c, img_n = res[("cuda", "render")].values, res[("native", "render")].values
 out["render_bitwise_equal"] = bool(np.array_equal(img_c, img_n))
 gc, gn = res[("cuda", "render_with_gradient")], res[("native", "render_with_gradient")]
