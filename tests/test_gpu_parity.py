@@ -527,3 +527,24 @@ def test_pose_group_order_is_invisible(cuda_device):
         assert torch.equal(i1[0], img[b])
         assert torch.equal(j1.view(6, H * W), jac[:, b])
         assert torch.equal(backward_from_jac(det, j1, g[b:b + 1].contiguous())[0], gf[b])
+
+
+def test_raysum_tangents_epilogue_matches_endpoint_contraction(golden, cuda_device):
+    """drr_raysum_tangents (the contraction in the walk's epilogue) equals the
+    reverse-mode endpoint derivatives contracted on the host, for the golden
+    kernel cases; empty ray bundles return empty arrays."""
+    be = _backend()
+    for c in range(0, int(golden["k_count"]), 7):
+        k = kernel_case(golden, c)
+        e, de = be.siddon_raysum_grad(k["flat"], k["dims"], k["spacing"], k["origin"],
+                                      k["source"], k["d_source"], k["pixels"], k["d_pixels"])
+        e2, gs, gp = be.ray_endpoint_grad(k["flat"], k["dims"], k["spacing"], k["origin"],
+                                          k["source"], k["pixels"])
+        np.testing.assert_array_equal(e, e2)
+        dpix = np.asarray(k["d_pixels"]).reshape(len(e), 3, -1)
+        ref = gs @ np.asarray(k["d_source"]) + np.einsum("na,nat->nt", gp, dpix)
+        scale = max(1.0, float(np.abs(ref).max()))
+        np.testing.assert_allclose(de, ref, rtol=0, atol=1e-13 * scale)
+    e, de = be.siddon_raysum_grad(k["flat"], k["dims"], k["spacing"], k["origin"], k["source"],
+                                  k["d_source"], np.zeros((0, 3)), np.zeros((0, 3, 7)))
+    assert e.shape == (0,) and de.shape == (0, 7)
