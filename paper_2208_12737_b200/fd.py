@@ -190,7 +190,7 @@ def ray_fd_report(vol: DeviceVolume, det: Detector, eta, steps=None, isocenter=N
     extrapolation (4 FD(h/2) - FD(h)) / 3 meets it is FD truncation error
     (O(h^2): a grazing ray's crossings curve fast), not a gradient error;
     ``unexplained`` counts the pairs that fail both."""
-    from .geometry import pose_frames
+    from .geometry import pixel_offsets, pose_frames
     from .renderer import render_frames, render_frames_jac
     eta = np.asarray(eta, dtype=np.float64).reshape(7)
     _check_pose(eta)
@@ -216,8 +216,7 @@ def ray_fd_report(vol: DeviceVolume, det: Detector, eta, steps=None, isocenter=N
     iso = vol.center if isocenter is None else tuple(float(v) for v in isocenter)
     Jf = torch.autograd.functional.jacobian(
         lambda e: pose_frames(e[None], iso)[0], torch.tensor(eta)).numpy()  # (12, 7)
-    ah = (np.arange(H) - (H - 1) / 2.0) * det.pitch_y
-    aw = (np.arange(W) - (W - 1) / 2.0) * det.pitch_x
+    ah, aw = (np.asarray(v) for v in pixel_offsets(H, W, det.pitch_x, det.pitch_y))
     dp = (Jf[3:6][None, None] + ah[:, None, None, None] * Jf[6:9][None, None]
           + aw[None, :, None, None] * Jf[9:12][None, None])  # (H, W, 3, 7)
     exact = (np.einsum("ahw,aj->hwj", jac[0:3], Jf[0:3])

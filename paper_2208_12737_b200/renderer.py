@@ -28,7 +28,8 @@ import torch
 
 from . import _lib
 from .errors import InvalidArgumentError
-from .geometry import check_gimbal, check_pose_vectors, pose_frames, volume_center
+from .geometry import (canonical_sdr_to_rho, check_gimbal, check_pose_vectors, pose_frames,
+                       volume_center)
 
 
 def _stream_ptr(device) -> int:
@@ -431,9 +432,7 @@ class DRR(torch.nn.Module):
         self.volume = DeviceVolume(volume, spacing, origin, device=device)
         self.detector = Detector(height, width if width is not None else height, delx, dely,
                                  ray_split=ray_split)
-        if not (float(sdr) > 0 and np.isfinite(float(sdr))):
-            raise InvalidArgumentError(f"sdr must be positive, got {sdr}")
-        self.sdr = float(sdr)
+        self.sdr = canonical_sdr_to_rho(float(sdr))
         self.isocenter = tuple(self.volume.center if isocenter is None else
                                (float(v) for v in isocenter))
         self.strict = strict
@@ -445,9 +444,8 @@ class DRR(torch.nn.Module):
         distributed.ShardedDRR): no upload, no copy."""
         self = cls.__new__(cls)
         torch.nn.Module.__init__(self)
-        if not (float(sdr) > 0 and np.isfinite(float(sdr))):
-            raise InvalidArgumentError(f"sdr must be positive, got {sdr}")
-        self.volume, self.detector, self.sdr = volume, detector, float(sdr)
+        self.volume, self.detector = volume, detector
+        self.sdr = canonical_sdr_to_rho(float(sdr))
         self.isocenter = tuple(volume.center if isocenter is None else
                                (float(v) for v in isocenter))
         self.strict = strict
