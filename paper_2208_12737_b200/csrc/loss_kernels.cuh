@@ -29,7 +29,10 @@ namespace drr {
 #endif
 constexpr int kLossThreads = DRR_LOSS_THREADS;
 constexpr int kLossCluster = 8;  // CTAs (SMs) per image
-constexpr int kLossBatch = 4;    // loads in flight per thread before they are summed (in order)
+#ifndef DRR_LOSS_BATCH
+#define DRR_LOSS_BATCH 4
+#endif
+constexpr int kLossBatch = DRR_LOSS_BATCH;  // loads in flight per thread before they are summed (in order)
 
 // Fixed-order block sum of five doubles: xor butterfly in each warp, then the
 // warps in index order; every thread returns the block totals.

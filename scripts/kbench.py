@@ -47,8 +47,13 @@ for B in [int(x) for x in (sys.argv[1:] or ["32", "1"])]:
     fns = {"fl": fused,
            "fwd": lambda: render_frames(drr.volume, drr.detector, frames),
            "bwd": lambda: backward_frames(drr.volume, drr.detector, frames, g),
-           "fj": lambda: hold.__setitem__(0, render_frames_jac(drr.volume, drr.detector, frames)[1]),
-           "bj": lambda: backward_from_jac(drr.detector, hold[0], g)}
+           "fj": lambda: hold.update(zip(("img", 0), render_frames_jac(drr.volume, drr.detector,
+                                                                        frames))),
+           "bj": lambda: backward_from_jac(drr.detector, hold[0], g),
+           "lgj": lambda: _lib.check(lib.drr_loss_grad_jac(
+               hold[0].data_ptr(), hold["img"].data_ptr(), fixed.data_ptr(), 0, 0, B,
+               drr.detector.c, _lib.DRR_LOSS_NEG_ZNCC, lb.value.data_ptr(), None,
+               lb.grad_frames.data_ptr(), None, None, torch.cuda.current_stream().cuda_stream))}
     hold = {}
     t = {k: [] for k in fns}
     for i in range(12):
@@ -60,7 +65,7 @@ for B in [int(x) for x in (sys.argv[1:] or ["32", "1"])]:
                 t[k].append(a.elapsed_time(b))
     m = {k: float(np.median(v)) for k, v in t.items()}
     res[B] = {"fused_loss_ms": m["fl"], "fwd_ms": m["fwd"], "bwd_ms": m["bwd"], "fwd_jac_ms": m["fj"], "bwd_jac_ms": m["bj"],
-              "steps_per_drr": S / B,
+              "loss_grad_jac_ms": m["lgj"], "steps_per_drr": S / B,
               "fwd_gsteps_s": S / m["fwd"] / 1e6, "fwd_jac_gsteps_s": S / m["fj"] / 1e6,
               "rewalk_drr_s": B / ((m["fwd"] + m["bwd"]) / 1e3),
               "one_walk_drr_s": B / ((m["fj"] + m["bj"]) / 1e3)}
