@@ -597,13 +597,14 @@ def main():
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f64 geometry / fp32 CT gathers",
+        "dtype": "f64",
         "data": "synthetic (chest-shaped CT phantom, SURVEY 8(d)); random narrow poses",
         "config": {"workload": WORKLOAD, "global_batch": GB, "poses_per_gpu": B,
                    "detector": [H, W], "ct": list(DIMS), "parallelism": f"pose-shard x{world}",
                    "collect": "per-pose loss + 7-gradient stored into rank 0's buffers by the "
                               "kernels (peer memory over NVLink), inside the timed region",
-                   "l2": "flushed (256 MiB write) between timed steps, outside the events"},
+                   "l2": "flushed (256 MiB write) between timed steps, outside the events",
+                   "arithmetic": "f64 geometry, crossings and sums; the CT stored and gathered as fp32"},
         "e2e": {"value": e2e_value, "unit": "DRR/s",
                 "h2d_bytes_per_step": int(GB * 7 * 8),
                 "d2h_bytes_per_step": int(GB * 8 * 8),
