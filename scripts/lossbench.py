@@ -1,4 +1,7 @@
-import torch, numpy as np, sys, os
+import os
+import sys
+
+import torch
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "."))
 from paper_2208_12737_b200 import _lib
 dev = torch.device("cuda")

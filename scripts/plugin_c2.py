@@ -10,7 +10,6 @@ chunks of 16384).  Measurement script (test infrastructure), not the product.
     PYTHONPATH=oracle/_ref:.:tests/ref_suite python scripts/plugin_c2.py
 """
 import json
-import math
 import os
 import sys
 import time
