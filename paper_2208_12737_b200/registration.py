@@ -209,6 +209,14 @@ def loss_and_gradient(vol: DeviceVolume, det: Detector, eta, fixed, loss_kind: s
         eta = eta[None]
     eta = eta.contiguous()
     B = eta.shape[0]
+    from .renderer import MAX_POSES_PER_LAUNCH
+    if B > MAX_POSES_PER_LAUNCH:  # one launch covers at most 65535 poses: chunk
+        per_pose = isinstance(fixed, (torch.Tensor, np.ndarray)) and fixed.ndim == 3
+        parts = [loss_and_gradient(vol, det, eta[lo:lo + MAX_POSES_PER_LAUNCH],
+                                   fixed[lo:lo + MAX_POSES_PER_LAUNCH] if per_pose else fixed,
+                                   loss_kind, isocenter, None, image_dtype, mode)
+                 for lo in range(0, B, MAX_POSES_PER_LAUNCH)]
+        return torch.cat([v for v, _ in parts]), torch.cat([g for _, g in parts])
     buf = (buffers if buffers is not None and buffers.B == B
            and buffers.image_dtype == image_dtype else _Buffers(vol, det, B, image_dtype, mode))
     fixed_t, stride = _prep_fixed(fixed, B, det, dev, image_dtype)

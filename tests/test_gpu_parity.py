@@ -435,10 +435,16 @@ def test_pose_batches_beyond_one_launch(golden, cuda_device, monkeypatch):
     g = torch.randn((frames.shape[0], 21, 21), device=cuda_device, dtype=torch.float64)
     whole = (render_frames(vol, det, frames), count_steps(vol, det, frames),
              backward_frames(vol, det, frames, g))
+    from paper_2208_12737_b200.registration import loss_and_gradient
+    eta = torch.tensor(golden["ps_poses"], device=cuda_device)
+    fixed = torch.rand((eta.shape[0], 21, 21), device=cuda_device)
+    whole_lg = loss_and_gradient(vol, det, eta, fixed)
     monkeypatch.setattr(renderer, "MAX_POSES_PER_LAUNCH", 2)
     split = (render_frames(vol, det, frames), count_steps(vol, det, frames),
              backward_frames(vol, det, frames, g))
     for a, b in zip(whole, split):
+        assert torch.equal(a, b)
+    for a, b in zip(whole_lg, loss_and_gradient(vol, det, eta, fixed)):
         assert torch.equal(a, b)
 
 
