@@ -240,9 +240,10 @@ class RegistrationEngine:
     ``mode="fused"`` (default): each iteration is ``drr_register_step`` --
     the Jacobian-free walk, the loss, and a reduction that also applies the
     momentum step and writes the next frames: three launches (C3 at C2, one
-    pose, one CUDA graph: 0.087 ms per step vs 0.094 with the six-launch
+    pose, one CUDA graph: 0.0854 ms per step vs 0.0880 for the four-launch
     stored-Jacobian iteration, ``scripts/c3_modes.py``).  ``mode="jac"``: the
-    stored-Jacobian chain + ``drr_register_update``."""
+    stored-Jacobian chain (pose frames, ``drr_forward_jac``,
+    ``drr_loss_grad_jac``) + ``drr_register_update``."""
 
     def __init__(self, vol: DeviceVolume, det: Detector, fixed, B: int = 1,
                  config: OptimizerConfig | None = None, isocenter=None,

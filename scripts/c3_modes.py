@@ -1,6 +1,7 @@
 """C3 (250-step registration on the C2 volume, one pose, whole loop one CUDA
-graph): ms per step with the stored-Jacobian iteration (6 launches) vs the
-three-launch drr_register_step iteration."""
+graph): ms per step with the stored-Jacobian iteration (4 launches: frames,
+forward_jac, loss_grad_jac, register_update) vs the three-launch
+drr_register_step iteration.  Last run: 0.0880 vs 0.0854 ms."""
 import json
 import math
 import os
