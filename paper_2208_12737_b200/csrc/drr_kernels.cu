@@ -846,7 +846,18 @@ __global__ void __launch_bounds__(kThreads)
 // chains it to dL/deta.  Replaces k_image_loss + k_backward_jac +
 // k_reduce_frames + k_pose_grad (four launches, and the fp32 pixel-gradient
 // round trip) for gradients.py:61-69 with the losses of metrics.py:71-91.
-template <typename IT>
+// Launch-time choice (drr_loss_grad_jac): the TMA-staged contraction when the
+// batch fills the GPU at least twice over (C2's 256 poses: 0.162 vs 0.197 ms),
+// else the register-staged one (32 poses: 0.033 vs 0.038 ms) --
+// scripts/gpu_lgj_tma.sh; both give the same bits.
+#ifndef DRR_LGJ_TMA
+#define DRR_LGJ_TMA 1
+#endif
+#ifndef DRR_LGJ_STAGES
+#define DRR_LGJ_STAGES 3
+#endif
+constexpr int kLgjStages = DRR_LGJ_STAGES;  // Jacobian tiles in flight per CTA (TMA path)
+template <typename IT, bool kTma>
 __global__ void __cluster_dims__(kLossCluster, 1, 1) __launch_bounds__(kLossThreads)
     k_loss_grad_jac(const double* __restrict__ jac, size_t npix_total, const IT* __restrict__ img,
                     const IT* __restrict__ fixed, int64_t fixed_stride, const DetDev det,
@@ -918,6 +929,100 @@ __global__ void __cluster_dims__(kLossCluster, 1, 1) __launch_bounds__(kLossThre
 #pragma unroll
   for (int k = 0; k < kFrameGrads; ++k) acc[k] = 0.0;
   const size_t pbase = static_cast<size_t>(b) * npix;
+  // one pixel's contribution, in the same order whichever way its six
+  // Jacobian entries arrived (thread t takes pixels lo + t, lo + t + T, ...)
+  auto contract = [&](int64_t i, double xa, double yb, const double* js, const double* jp) {
+    const double g = (c0 + c1 * xa) + c2 * yb;
+    const int h = static_cast<int>(i / det.W), w = static_cast<int>(i % det.W);
+    const double ah = (static_cast<double>(h) - det.half_h) * det.pitch_y;
+    const double aw = (static_cast<double>(w) - det.half_w) * det.pitch_x;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      acc[q] += g * js[q];
+      acc[3 + q] += g * jp[q];
+      acc[6 + q] += g * ah * jp[q];
+      acc[9 + q] += g * aw * jp[q];
+    }
+  };
+  if constexpr (kTma) {
+  // The Jacobian streams through shared memory: per tile of kLossThreads
+  // pixels, one thread issues six TMA bulk copies (one contiguous run per
+  // component, cp.async.bulk ... mbarrier::complete_tx) kLgjStages tiles
+  // ahead, so the loads in flight cost no registers (the register-staged
+  // form held 128 registers: 2 CTAs per SM, ~44% of HBM).  Tiles whose run
+  // is not 16-byte aligned / sized load directly.
+  {
+    __shared__ __align__(16) double stage[kLgjStages][6][kLossThreads];
+    __shared__ __align__(8) unsigned long long bars[kLgjStages];
+    const int64_t n = hi - lo;
+    const int ntiles = static_cast<int>((n + kLossThreads - 1) / kLossThreads);
+    const bool aligned = ((npix_total | (pbase + static_cast<size_t>(lo))) & 1) == 0;
+    const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+    const uint32_t stage0 = static_cast<uint32_t>(__cvta_generic_to_shared(&stage[0][0][0]));
+    auto tile_count = [&](int j) {
+      const int64_t c = n - static_cast<int64_t>(j) * kLossThreads;
+      return c < kLossThreads ? c : static_cast<int64_t>(kLossThreads);
+    };
+    auto tile_tma = [&](int j) { return aligned && (tile_count(j) & 1) == 0; };
+    auto issue = [&](int j) {  // one thread
+      if (j >= ntiles || !tile_tma(j)) return;
+      const int k = j % kLgjStages;
+      const uint32_t bytes = static_cast<uint32_t>(tile_count(j) * sizeof(double));
+      const uint32_t bar = bar0 + 8u * k;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"(6u * bytes) : "memory");
+      const size_t p0 = pbase + static_cast<size_t>(lo) + static_cast<size_t>(j) * kLossThreads;
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(stage0 + static_cast<uint32_t>(((k * 6 + q) * kLossThreads) * sizeof(double))),
+            "l"(jac + q * npix_total + p0), "r"(bytes), "r"(bar) : "memory");
+    };
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kLgjStages; ++k)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8u * k) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int j = 0; j < kLgjStages; ++j) issue(j);
+    for (int j = 0; j < ntiles; ++j) {
+      const int k = j % kLgjStages;
+      const int64_t i = lo + static_cast<int64_t>(j) * kLossThreads + threadIdx.x;
+      double js[3], jp[3];
+      // the two image values (L2-resident after the moment passes) are
+      // requested before waiting for the tile
+      const double xa = i < hi ? static_cast<double>(a[i]) : 0.0;
+      const double yb = i < hi ? static_cast<double>(f[i]) : 0.0;
+      if (tile_tma(j)) {
+        const uint32_t phase = static_cast<uint32_t>((j / kLgjStages) & 1);
+        asm volatile(
+            "{\n .reg .pred p;\n WAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            " @!p bra WAIT_%=;\n}\n" ::"r"(bar0 + 8u * k), "r"(phase) : "memory");
+        if (i < hi) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            js[q] = stage[k][q][threadIdx.x];
+            jp[q] = stage[k][3 + q][threadIdx.x];
+          }
+        }
+      } else if (i < hi) {
+        const size_t pix = pbase + static_cast<size_t>(i);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          js[q] = __ldg(jac + q * npix_total + pix);
+          jp[q] = __ldg(jac + (3 + q) * npix_total + pix);
+        }
+      }
+      if (i < hi) contract(i, xa, yb, js, jp);
+      __syncthreads();  // every thread is done with buffer k
+      if (threadIdx.x == 0) issue(j + kLgjStages);
+    }
+  }
+  } else {
   // kLossBatch pixels' loads in flight before any is accumulated (in order)
   for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += kLossThreads * kLossBatch) {
     double js[kLossBatch][3], jp[kLossBatch][3], xa[kLossBatch], yb[kLossBatch];
@@ -938,18 +1043,9 @@ __global__ void __cluster_dims__(kLossCluster, 1, 1) __launch_bounds__(kLossThre
     for (int u = 0; u < kLossBatch; ++u) {
       const int64_t i = i0 + static_cast<int64_t>(u) * kLossThreads;
       if (i >= hi) break;
-      const double g = (c0 + c1 * xa[u]) + c2 * yb[u];
-      const int h = static_cast<int>(i / det.W), w = static_cast<int>(i % det.W);
-      const double ah = (static_cast<double>(h) - det.half_h) * det.pitch_y;
-      const double aw = (static_cast<double>(w) - det.half_w) * det.pitch_x;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        acc[q] += g * js[u][q];
-        acc[3 + q] += g * jp[u][q];
-        acc[6 + q] += g * ah * jp[u][q];
-        acc[9 + q] += g * aw * jp[u][q];
-      }
+      contract(i, xa[u], yb[u], js[u], jp[u]);
     }
+  }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
@@ -1918,14 +2014,24 @@ int drr_loss_grad_jac(const double* d_jac, const void* d_img, const void* d_fixe
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   const dim3 grd(drr::kLossCluster, n_images);
   const size_t npix_total = static_cast<size_t>(n_images) * npix;
-  if (img_dtype == 0)
-    drr::k_loss_grad_jac<float><<<grd, drr::kLossThreads, 0, st>>>(
-        d_jac, npix_total, static_cast<const float*>(d_img), static_cast<const float*>(d_fixed),
-        fixed_stride, d, kind, d_value, d_status, d_grad_frames, d_eta, d_grad_eta);
-  else
-    drr::k_loss_grad_jac<double><<<grd, drr::kLossThreads, 0, st>>>(
-        d_jac, npix_total, static_cast<const double*>(d_img), static_cast<const double*>(d_fixed),
-        fixed_stride, d, kind, d_value, d_status, d_grad_frames, d_eta, d_grad_eta);
+  // TMA staging pays once the clusters fill the GPU twice (4 CTAs per SM)
+  const bool tma = DRR_LGJ_TMA && static_cast<int64_t>(n_images) * drr::kLossCluster >=
+                                      2 * 4 * static_cast<int64_t>(device_sms());
+  auto launch = [&](auto kern, const auto* img, const auto* fx) {
+    kern<<<grd, drr::kLossThreads, 0, st>>>(d_jac, npix_total, img, fx, fixed_stride, d, kind,
+                                            d_value, d_status, d_grad_frames, d_eta, d_grad_eta);
+  };
+  if (img_dtype == 0) {
+    const auto* im = static_cast<const float*>(d_img);
+    const auto* fx = static_cast<const float*>(d_fixed);
+    tma ? launch(drr::k_loss_grad_jac<float, true>, im, fx)
+        : launch(drr::k_loss_grad_jac<float, false>, im, fx);
+  } else {
+    const auto* im = static_cast<const double*>(d_img);
+    const auto* fx = static_cast<const double*>(d_fixed);
+    tma ? launch(drr::k_loss_grad_jac<double, true>, im, fx)
+        : launch(drr::k_loss_grad_jac<double, false>, im, fx);
+  }
   return check_launch("drr_loss_grad_jac");
 }
 

@@ -275,3 +275,36 @@ def test_loss_grad_jac_vs_oracle(cuda_device, kind):
             rge = rgf @ O.frame_jacobian(eta[i], vol.center)
             np.testing.assert_allclose(ge[i].cpu().numpy(), rge, rtol=0,
                                        atol=1e-9 * np.abs(rge).max())
+
+
+@pytest.mark.parametrize("img_f64", [False, True])
+def test_loss_grad_jac_tma_path_matches_register_path(cuda_device, img_f64):
+    """A batch large enough for drr_loss_grad_jac's TMA-staged contraction
+    (the Jacobian streamed through shared memory by bulk copies) gives the
+    bits of one-image calls, which take the register-staged path; odd image
+    sizes exercise the unaligned-tile fallbacks."""
+    from paper_2208_12737_b200 import Detector, DeviceVolume, _lib, pose_frames, render_frames_jac
+    vol = DeviceVolume(_volume(), SP, device=cuda_device)
+    det = Detector(37, 29, 3.0, 2.5, ray_split=1)
+    B = 2 * torch.cuda.get_device_properties(cuda_device).multi_processor_count + 3
+    et = torch.tensor(_poses(B, seed=21), device=cuda_device)
+    fr = pose_frames(et, vol.center).detach()
+    dt = torch.float64 if img_f64 else torch.float32
+    img, jac = render_frames_jac(vol, det, fr, out_dtype=dt)
+    fixed = torch.rand((B, 37, 29), device=cuda_device, dtype=dt)
+    npix = 37 * 29
+    lib = _lib.load()
+
+    def run(j, im, fx, n):
+        val = torch.empty(n, dtype=torch.float64, device=cuda_device)
+        gf = torch.empty((n, 12), dtype=torch.float64, device=cuda_device)
+        _lib.check(lib.drr_loss_grad_jac(j.data_ptr(), im.data_ptr(), fx.data_ptr(), int(img_f64),
+                                         npix, n, det.c, _lib.DRR_LOSS_NEG_ZNCC, val.data_ptr(),
+                                         None, gf.data_ptr(), None, None,
+                                         torch.cuda.current_stream().cuda_stream))
+        return val, gf
+    val, gf = run(jac, img, fixed, B)
+    for p in range(0, B, 7):
+        v1, g1 = run(jac[:, p * npix:(p + 1) * npix].contiguous(), img[p:p + 1].contiguous(),
+                     fixed[p:p + 1].contiguous(), 1)
+        assert torch.equal(v1[0], val[p]) and torch.equal(g1[0], gf[p]), p
