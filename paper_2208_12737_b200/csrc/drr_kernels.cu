@@ -998,10 +998,23 @@ __global__ void __cluster_dims__(kLossCluster, 1, 1) __launch_bounds__(kLossThre
       const double yb = i < hi ? static_cast<double>(f[i]) : 0.0;
       if (tile_tma(j)) {
         const uint32_t phase = static_cast<uint32_t>((j / kLgjStages) & 1);
+        // bounded wait: a tile that never lands (a bad address or byte
+        // count) traps after 2 s of wall time -- a launch error for the
+        // caller instead of a kernel that never retires
         asm volatile(
-            "{\n .reg .pred p;\n WAIT_%=:\n"
+            "{\n .reg .pred p;\n .reg .u64 t0, t1;\n"
             " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-            " @!p bra WAIT_%=;\n}\n" ::"r"(bar0 + 8u * k), "r"(phase) : "memory");
+            " @p bra DONE_%=;\n"
+            " mov.u64 t0, %%globaltimer;\n"
+            " WAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            " @p bra DONE_%=;\n"
+            " mov.u64 t1, %%globaltimer;\n"
+            " sub.u64 t1, t1, t0;\n"
+            " setp.gt.u64 p, t1, 2000000000;\n"
+            " @p trap;\n"
+            " bra WAIT_%=;\n"
+            " DONE_%=:\n}\n" ::"r"(bar0 + 8u * k), "r"(phase) : "memory");
         if (i < hi) {
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
