@@ -118,8 +118,8 @@ class _Buffers:
       pixel gradients (used for float64 images) and any batch size.
 
     ``"auto"`` takes ``"jac"`` for float32 images whose Jacobian fits
-    ``renderer.JAC_BUDGET_BYTES`` (C2: 256 poses = 0.5 GB), else ``"fused"``
-    (C5: 64 poses at 1024^2 would hold 3.2 GB)."""
+    ``renderer.JAC_BUDGET_BYTES`` (8 GiB; C2's 256 poses hold 0.5 GB, C5's 64
+    poses at 1024^2 3.2 GB), else ``"fused"``."""
 
     def __init__(self, vol: DeviceVolume, det: Detector, B: int, image_dtype=torch.float32,
                  mode: str = "auto"):
