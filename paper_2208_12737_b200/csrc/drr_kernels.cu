@@ -956,7 +956,10 @@ __global__ void __cluster_dims__(kLossCluster, 1, 1) __launch_bounds__(kLossThre
     __shared__ __align__(8) unsigned long long bars[kLgjStages];
     const int64_t n = hi - lo;
     const int ntiles = static_cast<int>((n + kLossThreads - 1) / kLossThreads);
-    const bool aligned = ((npix_total | (pbase + static_cast<size_t>(lo))) & 1) == 0;
+    // bulk copies need 16-byte aligned global runs: the Jacobian's base (any
+    // pointer a C-ABI caller passes) and every run's first element
+    const bool aligned = (reinterpret_cast<uintptr_t>(jac) & 15) == 0 &&
+                         ((npix_total | (pbase + static_cast<size_t>(lo))) & 1) == 0;
     const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
     const uint32_t stage0 = static_cast<uint32_t>(__cvta_generic_to_shared(&stage[0][0][0]));
     auto tile_count = [&](int j) {

@@ -278,21 +278,25 @@ def test_loss_grad_jac_vs_oracle(cuda_device, kind):
 
 
 @pytest.mark.parametrize("img_f64", [False, True])
-def test_loss_grad_jac_tma_path_matches_register_path(cuda_device, img_f64):
+@pytest.mark.parametrize("hw", [(37, 29), (90, 90)])
+def test_loss_grad_jac_tma_path_matches_register_path(cuda_device, img_f64, hw):
     """A batch large enough for drr_loss_grad_jac's TMA-staged contraction
     (the Jacobian streamed through shared memory by bulk copies) gives the
-    bits of one-image calls, which take the register-staged path; odd image
-    sizes exercise the unaligned-tile fallbacks."""
+    bits of one-image calls, which take the register-staged path.  37 x 29
+    (an odd batch of odd images): every tile falls back to direct loads;
+    90 x 90: 1013 pixels per CTA, so even ranks stream three full tiles by
+    TMA and load the odd last one directly, odd ranks start unaligned."""
     from paper_2208_12737_b200 import Detector, DeviceVolume, _lib, pose_frames, render_frames_jac
     vol = DeviceVolume(_volume(), SP, device=cuda_device)
-    det = Detector(37, 29, 3.0, 2.5, ray_split=1)
+    Hh, Ww = hw
+    det = Detector(Hh, Ww, 3.0 * 29 / Ww, 2.5 * 37 / Hh, ray_split=1)  # the same field
     B = 2 * torch.cuda.get_device_properties(cuda_device).multi_processor_count + 3
     et = torch.tensor(_poses(B, seed=21), device=cuda_device)
     fr = pose_frames(et, vol.center).detach()
     dt = torch.float64 if img_f64 else torch.float32
     img, jac = render_frames_jac(vol, det, fr, out_dtype=dt)
-    fixed = torch.rand((B, 37, 29), device=cuda_device, dtype=dt)
-    npix = 37 * 29
+    fixed = torch.rand((B, Hh, Ww), device=cuda_device, dtype=dt)
+    npix = Hh * Ww
     lib = _lib.load()
 
     def run(j, im, fx, n):
